@@ -1,0 +1,408 @@
+#!/usr/bin/env python
+"""bench.py -- GPU-AR next-reaction selections/sec on B200 (BASELINE.json metric).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config c4] [--impl gpuar|reference]
+
+One JSON line on rank 0.  Default workload (config c4, the per-realization K x M matrix
+named by BASELINE.json for 1/2/4/8 B200): M = 1029 yeast-like reactions, K = 2^20
+realizations PER GPU (weak scaling: each rank owns global rows [r*K, (r+1)*K), generated in
+its own HBM by libsynth -- no data-path collective).  A step is one gpuar_select over the
+K resident rows: per-row alpha_max / alpha_0 reductions, AR trials, tau (one kernel).
+The 4.3 GB matrix is > L2 (126 MB), so no L2 flush is needed between steps.
+
+--impl reference times the CPU oracle (oracle/, the parity reference) on rank 0 on a
+bounded sample of the same workload per step; the other ranks exit 0.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "next-reaction selections/sec at 1/2/4/8 B200; % of ALU/HBM roofline"
+UNIT = "selections/s"
+# fma-pipe IMAD throughput (B300_MICROARCH.md "Pipe rates": rt_SMSP = 2 -> 16 lanes/clk/SMSP)
+IMAD_PER_CLK_PER_SM = 64
+IMAD_PER_PHILOX = 20          # 10 rounds x 2 mul.wide.u32 (IMAD.WIDE.U32), checked in the SASS
+SM_COUNT = 148
+
+CONFIGS = {
+    "c1": dict(kind="shared", dist="hand", M=4, K=10_000,
+               desc="c1: M=4 hand-set {1,2,3,4}, K=10^4 selections, shared vector"),
+    "c2": dict(kind="shared", dist="yeast", M=1029, K=65_536,
+               desc="c2: M=1029 yeast-like shared vector in smem, K=65536 selections"),
+    "c3": dict(kind="shared", dist="pareto", M=10_000, K=1 << 20,
+               desc="c3: shared simulated distribution, K=2^20 selections"),
+    "c4": dict(kind="rows", dist="yeast", M=1029, K=1 << 20,
+               desc="c4: per-realization KxM matrix, M=1029 yeast-like rows, K=2^20 realizations per GPU"),
+    "c5": dict(kind="shared", dist="pareto", M=1_000_000, K=1 << 21,
+               desc="c5: M=1e6 Pareto(1.5) shared vector, K=2^21 selections per GPU (2^24 at 8 GPUs)"),
+}
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=1000)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="gpuar", choices=["gpuar", "reference"])
+    ap.add_argument("--config", default="c4", choices=sorted(CONFIGS))
+    ap.add_argument("--dist", default=None, help="c3: uniform|exponential|pareto")
+    ap.add_argument("--M", type=int, default=None)
+    ap.add_argument("--K", type=int, default=None, help="selections per GPU")
+    ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--cpu-seconds", type=float, default=10.0)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    return ap.parse_args()
+
+
+def workload(args) -> dict:
+    w = dict(CONFIGS[args.config])
+    if args.dist:
+        w["dist"] = args.dist
+    if args.M:
+        w["M"] = args.M
+    if args.K:
+        w["K"] = args.K
+    return w
+
+
+# ----------------------------------------------------------------- clocks during the timed region
+
+class ClockSampler:
+    FIELDS = ["index", "clocks.sm", "clocks.max.sm", "clocks_event_reasons.hw_slowdown",
+              "clocks_event_reasons.hw_thermal_slowdown", "clocks_event_reasons.sw_thermal_slowdown",
+              "clocks_event_reasons.sw_power_cap"]
+    NAMES = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+
+    def __init__(self, gpu_index: int):
+        self.gpu = gpu_index
+        self.rows = []
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--query-gpu={','.join(self.FIELDS)}", "--format=csv,noheader,nounits",
+                 "-i", str(self.gpu), "-lms", "50"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except FileNotFoundError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) == len(self.FIELDS):
+                self.rows.append((time.perf_counter(), parts))
+
+    def wait_first(self, timeout: float = 5.0) -> None:
+        t0 = time.perf_counter()
+        while self.proc and not self.rows and time.perf_counter() - t0 < timeout:
+            time.sleep(0.01)
+
+    def mark(self, start: float, end: float) -> None:
+        """Keep the samples taken inside [start, end] (plus the nearest one on each side)."""
+        inside = [r for r in self.rows if start <= r[0] <= end]
+        before = [r for r in self.rows if r[0] < start][-1:]
+        after = [r for r in self.rows if r[0] > end][:1]
+        self.window = before + inside + after
+
+    def __exit__(self, *exc):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self) -> dict:
+        rows = [r[1] for r in getattr(self, "window", [])]
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
+        sm = [float(r[1]) for r in rows if r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in rows if r[2].replace(".", "").isdigit()]
+        reasons = sorted({n for r in rows for n, v in zip(self.NAMES, r[3:]) if v.lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(rows)}
+
+
+# ----------------------------------------------------------------- helpers
+
+def measured_peaks() -> dict:
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            d = json.load(f)
+        d["_source"] = "measured"
+        return d
+    return {"hbm_gbs": 6650.0, "sm_max_mhz": 1965.0, "_source": "fallback"}
+
+
+def ncu_traffic(config: str):
+    """dram bytes per launch of the dominant kernel from the committed ncu --set full summary."""
+    p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if not os.path.exists(p):
+        return None
+    with open(p) as f:
+        d = json.load(f)
+    e = d.get(config)
+    return None if e is None else e.get("dram_bytes_per_launch")
+
+
+def make_inputs(w: dict, rank: int, device):
+    """Synthetic, seeded inputs (synth/) already resident in HBM."""
+    import numpy as np
+    import torch
+
+    import synth
+    M, K = w["M"], w["K"]
+    if w["kind"] == "rows":
+        import synth.gpu as sg
+        rates = torch.from_numpy(synth.yeast_rates(M)).to(device)
+        mat = torch.empty((K, M), dtype=torch.float32, device=device)
+        sg.fill_rows(mat, rates, synth.GEN_SEED, rank * K)
+        return mat
+    if w["dist"] == "hand":
+        a = synth.hand([1, 2, 3, 4])
+    else:
+        a = synth.distribution(w["dist"], M)
+    return torch.from_numpy(np.ascontiguousarray(a)).to(device)
+
+
+def host_sample(w: dict, rank: int, n: int):
+    import numpy as np
+
+    import synth
+    if w["kind"] == "rows":
+        return synth.rows(synth.yeast_rates(w["M"]), synth.GEN_SEED, rank * w["K"], n)
+    if w["dist"] == "hand":
+        return synth.hand([1, 2, 3, 4])
+    return np.ascontiguousarray(synth.distribution(w["dist"], w["M"]))
+
+
+def oracle_rate(w: dict, seconds: float, threads: int, max_rows: int | None = None):
+    """Oracle selections/s on a bounded sample of the workload (rank 0's first selections)."""
+    import oracle
+    probe = 256
+    K = w["K"]
+    while True:
+        n = min(probe, K)
+        alpha = host_sample(w, 0, n)
+        t0 = time.perf_counter()
+        oracle.ar_select(alpha, n, seed=20140327, nthreads=threads)
+        dt = time.perf_counter() - t0
+        if dt > 0.25 or n == K:
+            break
+        probe *= 4
+    target = int(n * seconds / max(dt, 1e-9))
+    n = max(1, min(K, target, max_rows or K))
+    alpha = host_sample(w, 0, n)
+    t0 = time.perf_counter()
+    oracle.ar_select(alpha, n, seed=20140327, nthreads=threads)
+    dt = time.perf_counter() - t0
+    return n / dt, n, dt
+
+
+# ----------------------------------------------------------------- the reference (oracle) arm
+
+def run_reference(args, w, rank, world):
+    if rank != 0:
+        return
+    threads = os.cpu_count() or 1
+    # each step: a bounded sample sized so the whole run takes ~2 minutes
+    budget = 120.0 / max(1, args.steps + args.warmup)
+    rate, n, _ = oracle_rate(w, budget, threads)
+    alpha = host_sample(w, 0, n)
+    import oracle
+    for _ in range(args.warmup):
+        oracle.ar_select(alpha, n, seed=20140327, nthreads=threads)
+    t0 = time.perf_counter()
+    for e in range(args.steps):
+        oracle.ar_select(alpha, n, seed=20140327, epoch=e, nthreads=threads)
+    dt = time.perf_counter() - t0
+    value = n * args.steps / dt
+    sample = f"{n} of the {w['K']} selections per step ({'rows' if w['kind'] == 'rows' else 'selections'} 0..{n - 1})"
+    out = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": dt / args.steps * 1e3,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+        "data": "synthetic", "config": {"workload": w["desc"], "M": w["M"], "K_per_gpu": w["K"]},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "oracle", "sample": sample},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(out), flush=True)
+
+
+# ----------------------------------------------------------------- our arm
+
+def run_gpuar(args, w, rank, world, local_rank):
+    import torch
+    import torch.distributed as dist
+
+    from paper_1404_0027_b200 import Selector
+
+    device = torch.device("cuda", local_rank)
+    torch.cuda.set_device(device)
+    M, K = w["M"], w["K"]
+    seed = 20140327
+    alpha = make_inputs(w, rank, device)
+    sel = Selector(M, K, seed, device=local_rank)
+    sel.set_selection_offset(rank * K)
+    if w["kind"] == "shared" and world > 1:
+        dist.broadcast(alpha, src=0)            # C1: one shared vector for all ranks
+    sel.set_propensities(alpha)
+    out = (torch.empty(K, dtype=torch.int32, device=device), torch.empty(K, dtype=torch.float32, device=device),
+           torch.empty(K, dtype=torch.int32, device=device))
+    for _ in range(max(args.warmup, 3)):
+        sel.select(K, out=out)
+    sel.sync()
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    stream = torch.cuda.current_stream(device)
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    path = sel.path
+    with ClockSampler(local_rank) as clk:
+        clk.wait_first()
+        for _ in range(max(args.warmup, 3)):      # re-warm after the sampler start-up
+            sel.select(K, out=out)
+        barrier()
+        t_start = time.perf_counter()
+        ev0.record(stream)
+        for _ in range(args.steps):
+            sel.select(K, out=out)
+        ev1.record(stream)
+        ev1.synchronize()
+        t_end = time.perf_counter()
+        time.sleep(0.06)
+        clk.mark(t_start, t_end)
+    barrier()
+    sel.sync()
+    ms = ev0.elapsed_time(ev1)
+    t = torch.tensor([ms], dtype=torch.float64, device=device)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)   # C3
+    ms_max = float(t.item())
+    ms_step = ms_max / args.steps
+    value = K * world * args.steps / (ms_max * 1e-3)
+
+    # validation of the last step (untimed): histogram (+ C2 reduce)
+    hist, totals = sel.histogram(out[0], out[2])
+    if world > 1:
+        dist.reduce(hist, dst=0)
+        dist.reduce(totals, dst=0)
+    trials_sum = int(totals[0].item())
+    rejected = int(totals[1].item())
+    calls = int(((out[2].to(torch.int64) + 1) // 2).sum().item()) + K   # Philox calls of the last launch
+
+    peaks = measured_peaks()
+    clocks = clk.summary()
+    if w["kind"] == "rows":
+        bytes_per_launch = K * (4 * M + 12)
+        achieved = bytes_per_launch / (ms_step * 1e-3) / 1e9
+        peak = float(peaks["hbm_gbs"])
+        traffic = ncu_traffic(args.config)
+        roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+                    "traffic": traffic, "peak_source": peaks["_source"] + " hbm_gbs (copy)",
+                    "bytes_per_selection": 4 * M + 12, "frac_of_8TBs": achieved / 8000.0}
+    else:
+        achieved = calls / (ms_step * 1e-3) / 1e9
+        mhz = float(peaks.get("sm_max_mhz", 1965.0))
+        peak = SM_COUNT * IMAD_PER_CLK_PER_SM / IMAD_PER_PHILOX * mhz * 1e6 / 1e9
+        roofline = {"bound": "alu", "achieved": achieved, "peak": peak, "unit": "G Philox calls/s",
+                    "frac": achieved / peak, "traffic": ncu_traffic(args.config),
+                    "peak_source": f"148 SM x 64 IMAD/clk / 20 IMAD per Philox4x32-10 x {mhz:.0f} MHz",
+                    "useful_trials_per_launch": trials_sum}
+
+    # e2e: host buffers through gpuar_select_host (H2D + select + D2H inside the timed region)
+    e2e = None
+    if not args.no_e2e:
+        if w["kind"] == "rows":
+            host = torch.empty((K, M), dtype=torch.float32, pin_memory=True)
+            host.copy_(alpha)
+            h2d = host.numel() * 4
+        else:
+            host = alpha.cpu().pin_memory()
+            h2d = host.numel() * 4
+        hout = tuple(torch.empty(K, dtype=dt, pin_memory=True) for dt in (torch.int32, torch.float32, torch.int32))
+        sel.select_host(host, K=K, out=hout)      # warm-up (allocates staging)
+        barrier()
+        t0 = time.perf_counter()
+        for _ in range(args.e2e_steps):
+            sel.select_host(host, K=K, out=hout)
+        dt = time.perf_counter() - t0
+        tt = torch.tensor([dt], dtype=torch.float64, device=device)
+        if world > 1:
+            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        e2e = {"value": K * world * args.e2e_steps / float(tt.item()), "unit": UNIT,
+               "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": 12 * K, "steps": args.e2e_steps,
+               "timer": "host wall clock around synchronous gpuar_select_host, max over ranks"}
+        del host
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        threads = os.cpu_count() or 1
+        rate, n, dt = oracle_rate(w, args.cpu_seconds, threads)
+        cpu = {"value": rate, "unit": UNIT, "cores": threads, "kind": "oracle",
+               "sample": f"first {n} of {K} selections of the same workload ({dt:.1f} s, OpenMP over selections)"}
+
+    if rank == 0:
+        res = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": max(args.warmup, 3), "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f32", "data": "synthetic (seeded synth/ generators)",
+            "config": {"workload": w["desc"], "M": M, "K_per_gpu": K, "K_total": K * world,
+                       "dist": w["dist"], "parallelism": f"selections sharded over {world} GPU(s), no data-path collective",
+                       "l2": ("inputs larger than L2 (%.2f GB/GPU), no flush" % (K * M * 4 / 1e9)) if w["kind"] == "rows"
+                       else "shared vector resident in smem/L2 by design; outputs 12 B/selection",
+                       "path": path},
+            "roofline": roofline,
+            "cpu_baseline": cpu,
+            "e2e": e2e,
+            "gpu_launches": args.steps,
+            "clocks": clocks,
+            "validation": {"trials_sum_last_step": trials_sum, "rejected_last_step": rejected,
+                           "mean_trials": trials_sum / (K * world)},
+        }
+        print(json.dumps(res), flush=True)
+    sel.close()
+
+
+def main():
+    args = parse()
+    w = workload(args)
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        run_reference(args, w, rank, world)
+        return
+    import torch
+    import torch.distributed as dist
+    if world > 1:
+        torch.cuda.set_device(local_rank)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    try:
+        run_gpuar(args, w, rank, world, local_rank)
+    finally:
+        if world > 1:
+            dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

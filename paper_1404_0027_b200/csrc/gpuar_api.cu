@@ -1,0 +1,541 @@
+// gpuar_api.cu -- libgpuar's C ABI (include/gpuar.h): handle, argument checks, launch
+// policy (which kernel, grid, shared-memory budget), stream ordering, sticky errors and
+// the host-buffer pipeline of gpuar_select_host.  No torch types anywhere: plain
+// pointers and sizes.
+#include <algorithm>
+#include <cmath>
+#include <cstdlib>
+#include <cstring>
+#include <new>
+
+#include "../../include/gpuar.h"
+#include "gpuar_internal.cuh"
+
+using namespace gpuar;
+
+namespace {
+
+constexpr int kRowsMaxWarps = 16;
+constexpr size_t kHostChunkBytes = 64ull << 20;  // gpuar_select_host row-chunk size
+
+struct Chunked {
+  float* stage[2] = {nullptr, nullptr};
+  size_t stage_floats = 0;
+  int32_t* idx = nullptr;
+  float* tau = nullptr;
+  uint32_t* trials = nullptr;
+  size_t out_cap = 0;
+  float* vec = nullptr;
+  size_t vec_cap = 0;
+  cudaStream_t s_in = nullptr, s_out = nullptr;
+  cudaEvent_t ev_in[2] = {nullptr, nullptr}, ev_comp[2] = {nullptr, nullptr};
+};
+
+int env_int(const char* name, int dflt) {
+  const char* v = std::getenv(name);
+  if (!v || !*v) return dflt;
+  return std::atoi(v);
+}
+
+}  // namespace
+
+struct gpuar_handle {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  int64_t M = 0, Kcap = 0;
+  uint64_t seed = 0;
+  uint32_t epoch = 0;
+  uint64_t offset = 0;
+  uint32_t max_trials = GPUAR_DEFAULT_MAX_TRIALS;
+  // registration
+  const float* alpha = nullptr;
+  int64_t rows = 0, ld = 0;
+  int path = kPathNone;
+  // device scratch
+  DevStats* d_stats = nullptr;
+  DevCounters* d_ctr = nullptr;
+  double* d_part_sum = nullptr;
+  uint32_t* d_part_max = nullptr;
+  int stats_blocks = 1;
+  uint16_t* d_pref = nullptr;
+  uint32_t n_pref = 0, group_shift = 0;
+  int shared_path = kPathSmemF32;  // which shared-vector path M implies
+  uint32_t shared_smem = 0;
+  // device properties
+  int num_sms = 148;
+  int smem_optin = 227 * 1024;
+  // rows policy
+  int rows_warps = 0, rows_stages = 0, rows_grid = 0;
+  uint32_t stage_bytes = 0;
+  // shared policy
+  int sh_block = 256, sh_grid = 0;
+  Chunked host;
+};
+
+namespace {
+
+struct DeviceGuard {
+  int prev = -1;
+  bool ok = true;
+  explicit DeviceGuard(int dev) {
+    if (cudaGetDevice(&prev) != cudaSuccess) prev = -1;
+    if (prev != dev) ok = cudaSetDevice(dev) == cudaSuccess;
+  }
+  ~DeviceGuard() {
+    if (prev >= 0) cudaSetDevice(prev);
+  }
+};
+
+int cuda_status(cudaError_t e) {
+  if (e == cudaSuccess) return GPUAR_OK;
+  if (e == cudaErrorMemoryAllocation) return GPUAR_ENOMEM;
+  return GPUAR_ECUDA;
+}
+
+// Which shared-vector path M implies, and its shared-memory footprint.
+void plan_shared(gpuar_handle* h) {
+  const uint64_t budget = (uint64_t)h->smem_optin - 1024u;
+  const uint64_t M = (uint64_t)h->M;
+  if (4u * M <= budget) {
+    h->shared_path = kPathSmemF32;
+    h->n_pref = 0;
+    h->group_shift = 0;
+    h->shared_smem = (uint32_t)((4u * M + 15u) & ~15ull);
+  } else if (2u * M <= budget) {
+    h->shared_path = kPathSmemBf16;
+    h->n_pref = (uint32_t)M;
+    h->group_shift = 0;
+    h->shared_smem = (uint32_t)((2u * M + 15u) & ~15ull);
+  } else {
+    uint32_t s = 1;
+    while (2u * ((M + (1ull << s) - 1) >> s) > budget) ++s;
+    h->shared_path = kPathSmemGroup;
+    h->group_shift = s;
+    h->n_pref = (uint32_t)((M + (1ull << s) - 1) >> s);
+    h->shared_smem = (uint32_t)((2u * h->n_pref + 15u) & ~15ull);
+  }
+  // block size maximising resident threads per SM
+  int best_threads = 0;
+  for (int block : {256, 512, 1024}) {
+    const int n = select_shared_blocks_per_sm(h->shared_path, block, h->shared_smem);
+    if (n * block > best_threads) {
+      best_threads = n * block;
+      h->sh_block = block;
+      h->sh_grid = n * h->num_sms;
+    }
+  }
+}
+
+// Rows ring: W warps x S slots of ceil16(4M) + 16 bytes (the 16-aligned cover of a row).
+int plan_rows(gpuar_handle* h) {
+  const uint64_t budget = (uint64_t)h->smem_optin - 1024u;
+  const uint64_t sb = ((4ull * (uint64_t)h->M + 15ull) & ~15ull) + 16ull;
+  int W = env_int("GPUAR_ROWS_WARPS", kRowsMaxWarps);
+  W = std::max(1, std::min(W, kRowsMaxWarps));
+  int S = env_int("GPUAR_ROWS_STAGES", 0);
+  auto fits = [&](int w, int s) { return (((uint64_t)w * s * 8u + 127u) & ~127ull) + (uint64_t)w * s * sb <= budget; };
+  if (S <= 0) {
+    S = 4;
+    while (S > 2 && !fits(W, S)) --S;
+  }
+  while (W > 1 && !fits(W, S)) --W;
+  if (!fits(W, S) || S > 32) return GPUAR_EINVAL;  // M too large for the row pipeline
+  h->rows_warps = W;
+  h->rows_stages = S;
+  h->stage_bytes = (uint32_t)sb;
+  const size_t sh = (((size_t)W * S * 8u + 127u) & ~(size_t)127u) + (size_t)W * S * sb;
+  const int n = select_rows_blocks_per_sm(W, sh);
+  if (n <= 0) return GPUAR_EINVAL;
+  h->rows_grid = n * h->num_sms;
+  return GPUAR_OK;
+}
+
+int launch_select(gpuar_handle* h, const float* alpha, int64_t rows, int64_t ld, int64_t K, uint64_t s0,
+                  int32_t* idx, float* tau, uint32_t* trials, cudaStream_t st) {
+  cudaError_t e;
+  if (rows == 1) {
+    SharedParams p{};
+    p.alpha = alpha;
+    p.prefilter = h->d_pref;
+    p.stats = h->d_stats;
+    p.ctr = h->d_ctr;
+    p.idx = idx;
+    p.tau = tau;
+    p.trials = trials;
+    p.M = (uint32_t)h->M;
+    p.K = (uint32_t)K;
+    p.s0 = (uint32_t)s0;
+    p.epoch = h->epoch;
+    p.seed_lo = (uint32_t)h->seed;
+    p.seed_hi = (uint32_t)(h->seed >> 32);
+    p.max_trials = h->max_trials;
+    p.n_pref = h->n_pref;
+    p.group_shift = h->group_shift;
+    p.smem_bytes = h->shared_smem;
+    e = launch_select_shared(p, h->shared_path, h->sh_grid, h->sh_block, st);
+  } else {
+    RowsParams p{};
+    p.alpha = alpha;
+    p.ctr = h->d_ctr;
+    p.idx = idx;
+    p.tau = tau;
+    p.trials = trials;
+    p.ld = (uint64_t)ld;
+    p.M = (uint32_t)h->M;
+    p.K = (uint32_t)K;
+    p.s0 = (uint32_t)s0;
+    p.epoch = h->epoch;
+    p.seed_lo = (uint32_t)h->seed;
+    p.seed_hi = (uint32_t)(h->seed >> 32);
+    p.max_trials = h->max_trials;
+    p.stages = (uint32_t)h->rows_stages;
+    p.stage_bytes = h->stage_bytes;
+    p.stats_only = 0;
+    const int grid = (int)std::min<int64_t>(h->rows_grid, (K + h->rows_warps - 1) / h->rows_warps);
+    e = launch_select_rows(p, std::max(grid, 1), h->rows_warps, st);
+  }
+  return cuda_status(e);
+}
+
+int check_err_flag(gpuar_handle* h) {
+  unsigned int err = 0;
+  cudaError_t e = cudaMemcpyAsync(&err, &h->d_ctr->err, sizeof(err), cudaMemcpyDeviceToHost, h->stream);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(h->stream);
+  if (e != cudaSuccess) return cuda_status(e);
+  if (err) {
+    e = cudaMemsetAsync(&h->d_ctr->err, 0, sizeof(unsigned int), h->stream);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(h->stream);
+    return e == cudaSuccess ? GPUAR_EPROPENSITY : cuda_status(e);
+  }
+  return GPUAR_OK;
+}
+
+int register_shared(gpuar_handle* h, const float* d_alpha) {
+  cudaError_t e = launch_stats(d_alpha, (uint32_t)h->M, h->d_part_sum, h->d_part_max, h->d_stats, h->d_ctr,
+                               h->stats_blocks, h->stream);
+  if (e == cudaSuccess && h->shared_path != kPathSmemF32)
+    e = launch_prefilter(d_alpha, (uint32_t)h->M, h->d_pref, h->n_pref, h->group_shift, h->shared_path, h->stream);
+  if (e != cudaSuccess) return cuda_status(e);
+  h->alpha = d_alpha;
+  h->rows = 1;
+  h->ld = h->M;
+  h->path = h->shared_path;
+  return GPUAR_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* gpuar_strerror(int status) {
+  switch (status) {
+    case GPUAR_OK: return "success";
+    case GPUAR_EINVAL: return "invalid argument";
+    case GPUAR_ENOMEM: return "out of memory";
+    case GPUAR_ECUDA: return "CUDA error";
+    case GPUAR_ENOTSET: return "propensities not set";
+    case GPUAR_EPROPENSITY: return "invalid propensity (negative, -0.0, NaN or Inf)";
+    default: return "unknown status";
+  }
+}
+
+int gpuar_create(gpuar_t* out, int64_t M, int64_t K, uint64_t seed) {
+  if (!out || M < 1 || M > 0x7fffffffll || K < 1 || K > 0xffffffffll) return GPUAR_EINVAL;
+  gpuar_handle* h = new (std::nothrow) gpuar_handle();
+  if (!h) return GPUAR_ENOMEM;
+  if (cudaGetDevice(&h->device) != cudaSuccess) {
+    delete h;
+    return GPUAR_ECUDA;
+  }
+  h->M = M;
+  h->Kcap = K;
+  h->seed = seed;
+  cudaDeviceGetAttribute(&h->num_sms, cudaDevAttrMultiProcessorCount, h->device);
+  cudaDeviceGetAttribute(&h->smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, h->device);
+  set_select_shared_limits(h->smem_optin);
+  set_select_rows_limits(h->smem_optin);
+  // stats launch shape depends on M only -> identical reduction tree on every rank
+  h->stats_blocks = (int)std::min<int64_t>((M + 4095) / 4096, 512);
+  plan_shared(h);
+  cudaError_t e = cudaMalloc(&h->d_stats, sizeof(DevStats));
+  if (e == cudaSuccess) e = cudaMalloc(&h->d_ctr, sizeof(DevCounters));
+  if (e == cudaSuccess) e = cudaMalloc(&h->d_part_sum, sizeof(double) * h->stats_blocks);
+  if (e == cudaSuccess) e = cudaMalloc(&h->d_part_max, sizeof(uint32_t) * h->stats_blocks);
+  if (e == cudaSuccess && h->n_pref) e = cudaMalloc(&h->d_pref, sizeof(uint16_t) * h->n_pref);
+  if (e == cudaSuccess) e = cudaMemset(h->d_ctr, 0, sizeof(DevCounters));
+  if (e == cudaSuccess) e = cudaMemset(h->d_stats, 0, sizeof(DevStats));
+  if (e == cudaSuccess) e = cudaDeviceSynchronize();
+  if (e != cudaSuccess) {
+    gpuar_destroy(h);
+    return cuda_status(e);
+  }
+  *out = h;
+  return GPUAR_OK;
+}
+
+int gpuar_destroy(gpuar_t h) {
+  if (!h) return GPUAR_OK;
+  DeviceGuard g(h->device);
+  cudaError_t e = cudaStreamSynchronize(h->stream);
+  Chunked& c = h->host;
+  if (c.s_in) cudaStreamSynchronize(c.s_in);
+  if (c.s_out) cudaStreamSynchronize(c.s_out);
+  for (int i = 0; i < 2; ++i) {
+    cudaFree(c.stage[i]);
+    if (c.ev_in[i]) cudaEventDestroy(c.ev_in[i]);
+    if (c.ev_comp[i]) cudaEventDestroy(c.ev_comp[i]);
+  }
+  cudaFree(c.idx);
+  cudaFree(c.tau);
+  cudaFree(c.trials);
+  cudaFree(c.vec);
+  if (c.s_in) cudaStreamDestroy(c.s_in);
+  if (c.s_out) cudaStreamDestroy(c.s_out);
+  cudaFree(h->d_stats);
+  cudaFree(h->d_ctr);
+  cudaFree(h->d_part_sum);
+  cudaFree(h->d_part_max);
+  cudaFree(h->d_pref);
+  delete h;
+  return e == cudaSuccess ? GPUAR_OK : GPUAR_ECUDA;
+}
+
+int gpuar_set_stream(gpuar_t h, void* stream) {
+  if (!h) return GPUAR_EINVAL;
+  h->stream = static_cast<cudaStream_t>(stream);
+  return GPUAR_OK;
+}
+
+int gpuar_set_propensities(gpuar_t h, const float* d_alpha, int64_t rows, int64_t ld) {
+  if (!h || !d_alpha) return GPUAR_EINVAL;
+  DeviceGuard g(h->device);
+  if (!g.ok) return GPUAR_ECUDA;
+  if (rows == 1) return register_shared(h, d_alpha);
+  if (rows < 1 || rows > h->Kcap || ld < h->M) return GPUAR_EINVAL;
+  if ((reinterpret_cast<uintptr_t>(d_alpha) & 15u) != 0) return GPUAR_EINVAL;
+  if (h->rows_warps == 0) {
+    const int st = plan_rows(h);
+    if (st != GPUAR_OK) return st;
+  }
+  h->alpha = d_alpha;
+  h->rows = rows;
+  h->ld = ld;
+  h->path = kPathRows;
+  return GPUAR_OK;
+}
+
+int gpuar_select(gpuar_t h, int64_t K, int32_t* d_idx, float* d_tau, uint32_t* d_trials) {
+  if (!h || !d_idx || K < 1 || K > h->Kcap) return GPUAR_EINVAL;
+  if (h->path == kPathNone) return GPUAR_ENOTSET;
+  if (h->rows != 1 && K != h->rows) return GPUAR_EINVAL;
+  if (h->offset + (uint64_t)K > (1ull << 32)) return GPUAR_EINVAL;
+  DeviceGuard g(h->device);
+  if (!g.ok) return GPUAR_ECUDA;
+  const int st = launch_select(h, h->alpha, h->rows, h->ld, K, h->offset, d_idx, d_tau, d_trials, h->stream);
+  if (st == GPUAR_OK) ++h->epoch;
+  return st;
+}
+
+int gpuar_select_host(gpuar_t h, const float* h_alpha, int64_t rows, int64_t ld, int64_t K, int32_t* h_idx,
+                      float* h_tau, uint32_t* h_trials) {
+  if (!h || !h_alpha || !h_idx || !h_tau || !h_trials || K < 1 || K > h->Kcap) return GPUAR_EINVAL;
+  if (!(rows == 1 || rows == K)) return GPUAR_EINVAL;
+  if (rows != 1 && ld < h->M) return GPUAR_EINVAL;
+  if (h->offset + (uint64_t)K > (1ull << 32)) return GPUAR_EINVAL;
+  DeviceGuard g(h->device);
+  if (!g.ok) return GPUAR_ECUDA;
+  Chunked& c = h->host;
+  cudaError_t e = cudaSuccess;
+  if (!c.s_in) {
+    e = cudaStreamCreateWithFlags(&c.s_in, cudaStreamNonBlocking);
+    if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&c.s_out, cudaStreamNonBlocking);
+    for (int i = 0; i < 2 && e == cudaSuccess; ++i) {
+      e = cudaEventCreateWithFlags(&c.ev_in[i], cudaEventDisableTiming);
+      if (e == cudaSuccess) e = cudaEventCreateWithFlags(&c.ev_comp[i], cudaEventDisableTiming);
+    }
+    if (e != cudaSuccess) return cuda_status(e);
+  }
+  if (c.out_cap < (size_t)K) {
+    cudaFree(c.idx);
+    cudaFree(c.tau);
+    cudaFree(c.trials);
+    c.idx = nullptr;
+    c.tau = nullptr;
+    c.trials = nullptr;
+    c.out_cap = 0;
+    e = cudaMalloc(&c.idx, 4 * K);
+    if (e == cudaSuccess) e = cudaMalloc(&c.tau, 4 * K);
+    if (e == cudaSuccess) e = cudaMalloc(&c.trials, 4 * K);
+    if (e != cudaSuccess) return cuda_status(e);
+    c.out_cap = (size_t)K;
+  }
+  int st = GPUAR_OK;
+  if (rows == 1) {
+    // shared vector: H2D of M floats, stats, select, D2H of the outputs
+    if (c.vec_cap < (size_t)h->M) {
+      cudaFree(c.vec);
+      c.vec = nullptr;
+      c.vec_cap = 0;
+      e = cudaMalloc(&c.vec, 4 * h->M);
+      if (e != cudaSuccess) return cuda_status(e);
+      c.vec_cap = (size_t)h->M;
+    }
+    e = cudaMemcpyAsync(c.vec, h_alpha, 4 * h->M, cudaMemcpyHostToDevice, h->stream);
+    if (e != cudaSuccess) return cuda_status(e);
+    st = register_shared(h, c.vec);
+    if (st == GPUAR_OK) st = launch_select(h, c.vec, 1, h->M, K, h->offset, c.idx, c.tau, c.trials, h->stream);
+    if (st != GPUAR_OK) return st;
+    e = cudaMemcpyAsync(h_idx, c.idx, 4 * K, cudaMemcpyDeviceToHost, h->stream);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(h_tau, c.tau, 4 * K, cudaMemcpyDeviceToHost, h->stream);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(h_trials, c.trials, 4 * K, cudaMemcpyDeviceToHost, h->stream);
+    if (e != cudaSuccess) return cuda_status(e);
+  } else {
+    if (h->rows_warps == 0) {
+      st = plan_rows(h);
+      if (st != GPUAR_OK) return st;
+    }
+    const int64_t R = std::max<int64_t>(1, std::min<int64_t>(K, (int64_t)(kHostChunkBytes / (4 * (size_t)ld))));
+    if (c.stage_floats < (size_t)(R * ld)) {
+      for (int i = 0; i < 2; ++i) {
+        cudaFree(c.stage[i]);
+        c.stage[i] = nullptr;
+      }
+      c.stage_floats = 0;
+      for (int i = 0; i < 2 && e == cudaSuccess; ++i) e = cudaMalloc(&c.stage[i], 4 * (size_t)R * ld);
+      if (e != cudaSuccess) return cuda_status(e);
+      c.stage_floats = (size_t)(R * ld);
+    }
+    // make the side streams start after everything already queued on the handle's stream
+    cudaEvent_t start = c.ev_comp[1];
+    e = cudaEventRecord(start, h->stream);
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(c.s_in, start, 0);
+    const int64_t nchunks = (K + R - 1) / R;
+    for (int64_t i = 0; i < nchunks && e == cudaSuccess; ++i) {
+      const int b = (int)(i & 1);
+      const int64_t r0 = i * R;
+      const int64_t nr = std::min<int64_t>(R, K - r0);
+      if (i >= 2) e = cudaStreamWaitEvent(c.s_in, c.ev_comp[b], 0);  // slot free
+      if (e == cudaSuccess)
+        e = cudaMemcpyAsync(c.stage[b], h_alpha + r0 * ld, 4 * (size_t)nr * ld, cudaMemcpyHostToDevice, c.s_in);
+      if (e == cudaSuccess) e = cudaEventRecord(c.ev_in[b], c.s_in);
+      if (e == cudaSuccess) e = cudaStreamWaitEvent(h->stream, c.ev_in[b], 0);
+      if (e != cudaSuccess) break;
+      st = launch_select(h, c.stage[b], nr, ld, nr, h->offset + r0, c.idx + r0, c.tau + r0, c.trials + r0,
+                         h->stream);
+      if (st != GPUAR_OK) return st;
+      e = cudaEventRecord(c.ev_comp[b], h->stream);
+      if (e == cudaSuccess) e = cudaStreamWaitEvent(c.s_out, c.ev_comp[b], 0);
+      if (e == cudaSuccess) e = cudaMemcpyAsync(h_idx + r0, c.idx + r0, 4 * nr, cudaMemcpyDeviceToHost, c.s_out);
+      if (e == cudaSuccess) e = cudaMemcpyAsync(h_tau + r0, c.tau + r0, 4 * nr, cudaMemcpyDeviceToHost, c.s_out);
+      if (e == cudaSuccess)
+        e = cudaMemcpyAsync(h_trials + r0, c.trials + r0, 4 * nr, cudaMemcpyDeviceToHost, c.s_out);
+    }
+    if (e == cudaSuccess) e = cudaStreamSynchronize(c.s_out);
+    if (e != cudaSuccess) return cuda_status(e);
+    h->alpha = nullptr;
+    h->path = kPathNone;
+    h->rows = 0;
+  }
+  ++h->epoch;
+  return check_err_flag(h);
+}
+
+int gpuar_set_selection_offset(gpuar_t h, int64_t s0) {
+  if (!h || s0 < 0 || s0 > 0xffffffffll) return GPUAR_EINVAL;
+  h->offset = (uint64_t)s0;
+  return GPUAR_OK;
+}
+
+int gpuar_set_epoch(gpuar_t h, uint32_t epoch) {
+  if (!h) return GPUAR_EINVAL;
+  h->epoch = epoch;
+  return GPUAR_OK;
+}
+
+int gpuar_get_epoch(gpuar_t h, uint32_t* epoch) {
+  if (!h || !epoch) return GPUAR_EINVAL;
+  *epoch = h->epoch;
+  return GPUAR_OK;
+}
+
+int gpuar_set_max_trials(gpuar_t h, uint32_t n) {
+  if (!h || n == 0) return GPUAR_EINVAL;
+  h->max_trials = n;
+  return GPUAR_OK;
+}
+
+int gpuar_get_stats(gpuar_t h, float* amax, double* a0, float* p) {
+  if (!h) return GPUAR_EINVAL;
+  if (h->path == kPathNone || h->rows != 1) return GPUAR_ENOTSET;
+  DeviceGuard g(h->device);
+  if (!g.ok) return GPUAR_ECUDA;
+  DevStats s;
+  cudaError_t e = cudaMemcpyAsync(&s, h->d_stats, sizeof(s), cudaMemcpyDeviceToHost, h->stream);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(h->stream);
+  if (e != cudaSuccess) return cuda_status(e);
+  const int st = check_err_flag(h);
+  if (st != GPUAR_OK) return st;
+  if (!s.valid) return GPUAR_EPROPENSITY;
+  float am;
+  std::memcpy(&am, &s.amax_bits, 4);
+  if (amax) *amax = am;
+  if (a0) *a0 = s.a0d;
+  if (p) *p = s.p;
+  return GPUAR_OK;
+}
+
+int gpuar_row_stats(gpuar_t h, float* d_amax, double* d_a0) {
+  if (!h || !d_amax || !d_a0) return GPUAR_EINVAL;
+  if (h->path != kPathRows) return GPUAR_ENOTSET;
+  DeviceGuard g(h->device);
+  if (!g.ok) return GPUAR_ECUDA;
+  RowsParams p{};
+  p.alpha = h->alpha;
+  p.ctr = h->d_ctr;
+  p.amax_out = d_amax;
+  p.a0_out = d_a0;
+  p.ld = (uint64_t)h->ld;
+  p.M = (uint32_t)h->M;
+  p.K = (uint32_t)h->rows;
+  p.max_trials = h->max_trials;
+  p.stages = (uint32_t)h->rows_stages;
+  p.stage_bytes = h->stage_bytes;
+  p.stats_only = 1;
+  const int grid = (int)std::min<int64_t>(h->rows_grid, (h->rows + h->rows_warps - 1) / h->rows_warps);
+  return cuda_status(launch_select_rows(p, std::max(grid, 1), h->rows_warps, h->stream));
+}
+
+int gpuar_sync(gpuar_t h) {
+  if (!h) return GPUAR_EINVAL;
+  DeviceGuard g(h->device);
+  if (!g.ok) return GPUAR_ECUDA;
+  cudaError_t e = cudaStreamSynchronize(h->stream);
+  if (e != cudaSuccess) return cuda_status(e);
+  return check_err_flag(h);
+}
+
+int gpuar_histogram(gpuar_t h, const int32_t* d_idx, const uint32_t* d_trials, int64_t K, uint64_t* d_hist,
+                    uint64_t* d_totals) {
+  if (!h || !d_idx || !d_hist || !d_totals || K < 1 || K > 0xffffffffll) return GPUAR_EINVAL;
+  DeviceGuard g(h->device);
+  if (!g.ok) return GPUAR_ECUDA;
+  return cuda_status(launch_histogram(d_idx, d_trials, (uint32_t)K, (uint32_t)h->M,
+                                      reinterpret_cast<unsigned long long*>(d_hist),
+                                      reinterpret_cast<unsigned long long*>(d_totals), h->num_sms * 4, h->stream));
+}
+
+int gpuar_bench_philox(gpuar_t h, int64_t n_threads, int32_t calls, uint32_t* d_sink) {
+  if (!h || !d_sink || n_threads < 1 || n_threads > 0x7fffffffll || calls < 1) return GPUAR_EINVAL;
+  DeviceGuard g(h->device);
+  if (!g.ok) return GPUAR_ECUDA;
+  return cuda_status(launch_bench_philox((uint32_t)n_threads, (uint32_t)calls, (uint32_t)h->seed,
+                                         (uint32_t)(h->seed >> 32), d_sink, h->stream));
+}
+
+int gpuar_path(gpuar_t h, int32_t* path) {
+  if (!h || !path) return GPUAR_EINVAL;
+  *path = h->path;
+  return GPUAR_OK;
+}
+
+}  // extern "C"

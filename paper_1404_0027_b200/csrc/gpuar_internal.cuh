@@ -1,0 +1,154 @@
+// gpuar_internal.cuh -- device-side structures, PTX helpers and kernel launchers shared
+// by libgpuar's translation units.  Not part of the ABI (include/gpuar.h is).
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace gpuar {
+
+constexpr uint32_t kFull = 0xffffffffu;
+constexpr uint32_t kNone = 0xffffffffu;
+constexpr uint32_t kInfBits = 0x7f800000u;   // a valid propensity's bits are < this
+
+// Shared-vector statistics (written by the stats kernel, read by the select kernels).
+struct DevStats {
+  uint32_t amax_bits;  // bits of alpha_max = max over uint bits (order-free, exact)
+  uint32_t valid;      // 1 iff every bit pattern < 0x7f800000 (+0 or positive finite)
+  float a0f;           // fl32(alpha_0)
+  float p;             // alpha_0 / (M alpha_max), 0 if alpha_max == 0
+  double a0d;          // alpha_0 in binary64, fixed reduction tree
+  uint32_t grab;       // work-stealing chunk (selections per atomic grab)
+  uint32_t pad;
+};
+
+// Per-handle device counters.
+struct DevCounters {
+  unsigned long long next;  // work-stealing ticket (reset by the last CTA of each launch)
+  unsigned int done;        // CTAs finished in the current launch
+  unsigned int err;         // sticky EPROPENSITY flag (cleared by the host)
+};
+
+enum Path : int {
+  kPathNone = 0,
+  kPathSmemF32 = 1,    // shared vector fully in shared memory (binary32)
+  kPathSmemBf16 = 2,   // shared vector: per-element bf16 truncation bracket in smem, exact in L2
+  kPathSmemGroup = 3,  // shared vector: bf16 round-up group maxima in smem, exact in L2
+  kPathRows = 4,       // per-realization K x M matrix, bulk-async staged rows
+};
+
+struct SharedParams {
+  const float* alpha;        // M floats (device)
+  const uint16_t* prefilter; // paths 2/3: bf16 codes (device)
+  const DevStats* stats;
+  DevCounters* ctr;
+  int32_t* idx;
+  float* tau;
+  uint32_t* trials;
+  uint32_t M;
+  uint32_t K;
+  uint32_t s0;
+  uint32_t epoch;
+  uint32_t seed_lo, seed_hi;
+  uint32_t max_trials;
+  uint32_t n_pref;           // number of prefilter entries (paths 2/3)
+  uint32_t group_shift;      // path 3: log2(group size)
+  uint32_t smem_bytes;       // bytes of the staged vector / prefilter
+};
+
+struct RowsParams {
+  const float* alpha;        // K rows, pitch ld floats, 16-byte aligned base
+  DevCounters* ctr;
+  int32_t* idx;
+  float* tau;
+  uint32_t* trials;
+  float* amax_out;           // gpuar_row_stats only
+  double* a0_out;            // gpuar_row_stats only
+  uint64_t ld;
+  uint32_t M;
+  uint32_t K;
+  uint32_t s0;
+  uint32_t epoch;
+  uint32_t seed_lo, seed_hi;
+  uint32_t max_trials;
+  uint32_t stages;           // ring depth per warp
+  uint32_t stage_bytes;      // bytes per ring slot (multiple of 16)
+  uint32_t stats_only;       // 1: gpuar_row_stats (no trials)
+};
+
+// ---------------------------------------------------------------- PTX helpers
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+               : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  const uint32_t a = smem_u32(bar);
+  asm volatile(
+      "{\n"
+      ".reg .pred P1;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+      "@!P1 bra WAIT_%=;\n"
+      "}\n" ::"r"(a),
+      "r"(parity)
+      : "memory");
+}
+
+// 1-D bulk async copy global -> shared (SASS UBLKCP), completion counted on `bar`.
+// dst, src 16-byte aligned; bytes a multiple of 16.  L2 policy evict_first: every
+// propensity row is read exactly once.
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar,
+                                         uint64_t policy) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(policy)
+      : "memory");
+}
+
+__device__ __forceinline__ uint64_t policy_evict_first() {
+  uint64_t pol;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+  return pol;
+}
+
+__device__ __forceinline__ void fence_proxy_async_smem() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+
+__device__ __forceinline__ uint32_t lanemask_lt() {
+  uint32_t m;
+  asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
+  return m;
+}
+
+// ---------------------------------------------------------------- launchers (host)
+
+cudaError_t launch_stats(const float* alpha, uint32_t M, double* part_sum, uint32_t* part_max,
+                         DevStats* stats, DevCounters* ctr, int stats_blocks, cudaStream_t st);
+cudaError_t launch_prefilter(const float* alpha, uint32_t M, uint16_t* pref, uint32_t n_pref,
+                             uint32_t group_shift, int path, cudaStream_t st);
+cudaError_t launch_select_shared(const SharedParams& p, int path, int grid, int block, cudaStream_t st);
+cudaError_t launch_select_rows(const RowsParams& p, int grid, int warps, cudaStream_t st);
+cudaError_t launch_histogram(const int32_t* idx, const uint32_t* trials, uint32_t K, uint32_t M,
+                             unsigned long long* hist, unsigned long long* totals, int grid,
+                             cudaStream_t st);
+cudaError_t launch_bench_philox(uint32_t n_threads, uint32_t calls, uint32_t seed_lo, uint32_t seed_hi,
+                                uint32_t* sink, cudaStream_t st);
+
+// Occupancy helpers (filled by the TU owning each kernel).
+int select_shared_blocks_per_sm(int path, int block, size_t smem);
+int select_rows_blocks_per_sm(int warps, size_t smem);
+void set_select_shared_limits(int bytes);
+void set_select_rows_limits(int bytes);
+
+}  // namespace gpuar

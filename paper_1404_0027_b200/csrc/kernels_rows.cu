@@ -1,0 +1,179 @@
+// kernels_rows.cu -- GPU-AR selection over a per-realization K x M propensity matrix
+// (config c4: M = 1029, K = 2^20, 4.02 GiB): row k = D[k*ld + j] is
+// realization k's propensity vector, so each row needs its own alpha_max / alpha_0
+// before its trials.
+//
+// The row must be read once in full (alpha_0 needs every alpha_j), so the kernel is
+// HBM-bound: 4M bytes per selection is the algorithmic minimum.  Design:
+//  * persistent CTAs, W warps each; every warp owns a private ring of S row slots in
+//    shared memory and its own mbarriers -- it is its own producer (lane 0 issues a 1-D
+//    bulk async copy, cp.async.bulk -> SASS UBLKCP, of the row's 16-byte-aligned cover)
+//    and consumer, so a slow row (geometric trial count) never stalls another warp;
+//  * rows are streamed with an L2 evict_first policy (read exactly once);
+//  * per row: warp-wide max of the bit patterns (exact alpha_max + validity) and
+//    alpha_0 as binary32 pairwise sums of 8 promoted to binary64 (error <= 4u relative,
+//    DESIGN.md R11), then trials in rounds of 32 Philox calls = 64 trials per warp with a
+//    ballot/__ffs first-accept, then tau with -ln(u1) precomputed 32 rows at a time.
+// Row 4116 bytes is not a multiple of 16, so no 2-D tensor map can describe the matrix;
+// each row's copy covers [floor16(start), ceil16(end)) -- at most 15 extra bytes on
+// each side, always inside 16-byte chunks that hold row data.
+#include <algorithm>
+
+#include "gpuar_internal.cuh"
+#include "philox.cuh"
+
+namespace gpuar {
+
+namespace {
+
+constexpr uint32_t kMaxWarps = 16;
+
+__global__ void __launch_bounds__(kMaxWarps * 32, 1) select_rows_kernel(const RowsParams P) {
+  extern __shared__ __align__(128) unsigned char smem[];
+  const uint32_t warps = blockDim.x >> 5;
+  const uint32_t warp = threadIdx.x >> 5;
+  const uint32_t lane = threadIdx.x & 31u;
+  const uint32_t S = P.stages;
+  const uint32_t SB = P.stage_bytes;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem) + warp * S;
+  unsigned char* ring = smem + ((warps * S * 8u + 127u) & ~127u) + (size_t)warp * S * SB;
+
+  if (lane < S) mbar_init(&bars[lane], 1u);
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  __syncwarp();
+
+  const uint64_t policy = policy_evict_first();
+  const uint64_t G = gridDim.x;
+  const uint64_t K = P.K;
+  const uint32_t M = P.M;
+  const uint64_t row_bytes = P.ld * 4ull;
+  // row handled by this warp at its n-th step: CTAs take consecutive blocks of W rows
+  auto row_of = [&](uint32_t n) -> uint64_t { return ((uint64_t)n * G + blockIdx.x) * warps + warp; };
+  auto issue = [&](uint32_t n, uint32_t slot) {
+    const uint64_t off = row_of(n) * row_bytes;
+    const uint64_t a = off & ~15ull;
+    const uint64_t e = (off + 4ull * M + 15ull) & ~15ull;
+    const uint32_t bytes = (uint32_t)(e - a);
+    mbar_arrive_expect_tx(&bars[slot], bytes);
+    bulk_g2s(ring + (size_t)slot * SB, reinterpret_cast<const unsigned char*>(P.alpha) + a, bytes, &bars[slot],
+             policy);
+  };
+  if (lane == 0) {
+    for (uint32_t s = 0; s < S; ++s)
+      if (row_of(s) < K) issue(s, s);
+  }
+
+  const uint32_t half = P.max_trials >> 1;
+  const uint32_t calls = half + (P.max_trials & 1u);
+  const uint32_t full_chunks = M >> 8;  // 256 elements = 8 per lane
+  float nlog = 0.f;                     // -ln(u1) of row_of(n0 + lane)
+
+  for (uint32_t n = 0;; ++n) {
+    const uint64_t r = row_of(n);
+    if (r >= K) break;
+    const uint32_t slot = n % S;
+    const uint32_t parity = (n / S) & 1u;
+    if ((n & 31u) == 0u && !P.stats_only) {
+      const uint64_t rr = row_of(n + lane);
+      nlog = rr < K ? neg_log_u1(P.seed_lo, P.seed_hi, P.s0 + (uint32_t)rr, P.epoch) : 0.f;
+    }
+    mbar_wait(&bars[slot], parity);
+    const float* row = reinterpret_cast<const float*>(ring + (size_t)slot * SB + ((r * row_bytes) & 15ull));
+
+    // ---- alpha_max (max of bit patterns) and alpha_0
+    uint32_t mx = 0;
+    double acc = 0.0;
+    for (uint32_t ch = 0; ch < full_chunks; ++ch) {
+      const float* p = row + ch * 256u + lane;
+      float v[8];
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        v[k] = p[k * 32];
+        mx = max(mx, __float_as_uint(v[k]));
+      }
+      const float s = __fadd_rn(__fadd_rn(__fadd_rn(v[0], v[1]), __fadd_rn(v[2], v[3])),
+                                __fadd_rn(__fadd_rn(v[4], v[5]), __fadd_rn(v[6], v[7])));
+      acc += (double)s;
+    }
+    {
+      float s = 0.f;  // tail: at most 8 elements per lane, sequential
+      for (uint32_t j = (full_chunks << 8) + lane; j < M; j += 32u) {
+        const float v = row[j];
+        mx = max(mx, __float_as_uint(v));
+        s = __fadd_rn(s, v);
+      }
+      acc += (double)s;
+    }
+    mx = __reduce_max_sync(kFull, mx);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(kFull, acc, o);
+
+    if (P.stats_only) {
+      if (lane == 0) {
+        P.amax_out[r] = mx < kInfBits ? __uint_as_float(mx) : __uint_as_float(0x7fc00000u);
+        P.a0_out[r] = mx < kInfBits ? acc : __longlong_as_double(0x7ff8000000000000ll);
+      }
+    } else {
+      const float nl = __shfl_sync(kFull, nlog, n & 31u);
+      int32_t id = -1;
+      uint32_t tr = 0;
+      float tau;
+      if (mx >= kInfBits) {  // invalid row: sticky EPROPENSITY
+        tau = __uint_as_float(0x7fc00000u);
+        if (lane == 0) atomicOr(&P.ctr->err, 1u);
+      } else if (mx == 0u) {  // all-zero row: nothing can fire
+        tau = __uint_as_float(kInfBits);
+      } else {
+        const float amax = __uint_as_float(mx);
+        tau = __fdiv_rn(nl, __double2float_rn(acc));
+        tr = P.max_trials;
+        const uint32_t sg = P.s0 + (uint32_t)r;
+        for (uint32_t c0 = 0; c0 < calls; c0 += 32u) {
+          const uint32_t c = c0 + lane;
+          const Philox4 x = philox4x32_10(c, sg, P.epoch, kTagTrials, P.seed_lo, P.seed_hi);
+          const uint32_t j0 = __umulhi(x.x, M);
+          const uint32_t j1 = __umulhi(x.z, M);
+          const bool a0 = c < calls && __fmul_rn(unit24(x.y), amax) < row[j0];
+          const bool a1 = !a0 && c < half && __fmul_rn(unit24(x.w), amax) < row[j1];
+          const uint32_t b = __ballot_sync(kFull, a0 || a1);
+          if (b != 0u) {
+            const uint32_t w = __ffs(b) - 1;
+            id = (int32_t)__shfl_sync(kFull, a0 ? j0 : j1, w);
+            tr = __shfl_sync(kFull, a0 ? 2u * c + 1u : 2u * c + 2u, w);
+            break;
+          }
+        }
+      }
+      if (lane == 0) {
+        P.idx[r] = id;
+        if (P.tau) P.tau[r] = tau;
+        if (P.trials) P.trials[r] = tr;
+      }
+    }
+    __syncwarp();
+    if (lane == 0 && row_of(n + S) < K) {
+      fence_proxy_async_smem();  // generic-proxy reads of the slot precede the async refill
+      issue(n + S, slot);
+    }
+  }
+}
+
+}  // namespace
+
+cudaError_t launch_select_rows(const RowsParams& p, int grid, int warps, cudaStream_t st) {
+  const size_t sh = (((size_t)warps * p.stages * 8u + 127u) & ~(size_t)127u) + (size_t)warps * p.stages * p.stage_bytes;
+  select_rows_kernel<<<grid, warps * 32, sh, st>>>(p);
+  return cudaGetLastError();
+}
+
+int select_rows_blocks_per_sm(int warps, size_t smem) {
+  int n = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, select_rows_kernel, warps * 32, smem) != cudaSuccess) return 0;
+  return n;
+}
+
+void set_select_rows_limits(int bytes) {
+  cudaFuncSetAttribute(select_rows_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+}
+
+}  // namespace gpuar

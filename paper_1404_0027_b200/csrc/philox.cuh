@@ -1,0 +1,61 @@
+// philox.cuh -- Philox4x32-10 in registers (Salmon et al., SC'11), the counter-based
+// stream BASELINE.json's north_star fixes for GPU-AR.  The paper instead filled a K x M
+// array of uniforms in global memory with a third-party generator (PAPER.md:455-459,
+// 713-714); a counter-based generator needs no storage and makes every selection's
+// draws a pure function of (seed, selection, epoch, call).
+#pragma once
+#include <cstdint>
+
+namespace gpuar {
+
+constexpr uint32_t kPhiloxM0 = 0xD2511F53u;
+constexpr uint32_t kPhiloxM1 = 0xCD9E8D57u;
+constexpr uint32_t kPhiloxW0 = 0x9E3779B9u;
+constexpr uint32_t kPhiloxW1 = 0xBB67AE85u;
+
+// Stream tags (counter word 3), R12.
+constexpr uint32_t kTagTrials = 0u;
+constexpr uint32_t kTagTau = 1u;
+
+struct Philox4 {
+  uint32_t x, y, z, w;
+};
+
+// Ten rounds of (hi0,lo0) = M0*c0, (hi1,lo1) = M1*c2, c = (hi1^c1^k0, lo1, hi0^c3^k1, lo0),
+// key += Weyl between rounds.  Fully unrolled; mul.wide.u32 gives hi and lo in one
+// IMAD.WIDE.U32.
+__device__ __forceinline__ Philox4 philox4x32_10(uint32_t c0, uint32_t c1, uint32_t c2, uint32_t c3,
+                                                 uint32_t k0, uint32_t k1) {
+#pragma unroll
+  for (int r = 0; r < 10; ++r) {
+    const uint64_t p0 = (uint64_t)kPhiloxM0 * c0;
+    const uint64_t p1 = (uint64_t)kPhiloxM1 * c2;
+    const uint32_t hi0 = (uint32_t)(p0 >> 32), lo0 = (uint32_t)p0;
+    const uint32_t hi1 = (uint32_t)(p1 >> 32), lo1 = (uint32_t)p1;
+    c0 = hi1 ^ c1 ^ k0;
+    c1 = lo1;
+    c2 = hi0 ^ c3 ^ k1;
+    c3 = lo0;
+    k0 += kPhiloxW0;
+    k1 += kPhiloxW1;
+  }
+  return Philox4{c0, c1, c2, c3};
+}
+
+// u = (x >> 8) * 2^-24 in [0,1): 24 random bits, exact in binary32 (R3).
+__device__ __forceinline__ float unit24(uint32_t x) {
+  return __fmul_rn(__uint2float_rn(x >> 8), 0x1p-24f);
+}
+
+// u1 = (2 (x >> 9) + 1) * 2^-24 in (0,1) (R10).
+__device__ __forceinline__ float unit24_open(uint32_t x) {
+  return __fmul_rn(__uint2float_rn(((x >> 9) << 1) | 1u), 0x1p-24f);
+}
+
+// tau = ln(1/u1) / alpha_0 in binary32: -logf(u1) / a0f.
+__device__ __forceinline__ float neg_log_u1(uint32_t seed_lo, uint32_t seed_hi, uint32_t s, uint32_t epoch) {
+  const Philox4 t = philox4x32_10(0u, s, epoch, kTagTau, seed_lo, seed_hi);
+  return -logf(unit24_open(t.x));
+}
+
+}  // namespace gpuar

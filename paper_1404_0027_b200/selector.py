@@ -1,0 +1,196 @@
+"""Thin Python binding over libgpuar (include/gpuar.h): the same operations under the same
+names, with torch tensors for device memory and torch's current CUDA stream.  Argument
+marshalling only -- every step of the selection runs in the library's CUDA kernels.
+"""
+from __future__ import annotations
+
+import ctypes
+
+import numpy as np
+import torch
+
+from . import _abi
+from ._abi import check
+
+PATHS = {0: "none", 1: "smem_f32", 2: "smem_bf16_bracket", 3: "smem_group_max", 4: "rows"}
+
+
+def _ptr(t: torch.Tensor | None):
+    return None if t is None else ctypes.c_void_p(t.data_ptr())
+
+
+class Selector:
+    """GPU-AR selector for M reactions and up to K selections per call (gpuar_create).
+
+    Usage::
+
+        sel = Selector(M, K, seed)
+        sel.set_propensities(alpha)          # (M,) shared vector or (K, ld) matrix, cuda fp32
+        idx, tau, trials = sel.select()      # gpuar_select, epoch += 1
+    """
+
+    def __init__(self, M: int, K: int, seed: int, device: int | torch.device | None = None):
+        self._lib = _abi.load()
+        if device is None:
+            index = torch.cuda.current_device()
+        elif isinstance(device, int):
+            index = device
+        else:
+            index = torch.device(device).index or 0
+        self.device = torch.device("cuda", index)
+        self.M, self.K, self.seed = int(M), int(K), int(seed)
+        h = ctypes.c_void_p()
+        with torch.cuda.device(self.device):
+            check(self._lib.gpuar_create(ctypes.byref(h), self.M, self.K, self.seed & (2**64 - 1)), "gpuar_create")
+        self._h = h
+        self._alpha = None      # keeps the borrowed propensity tensor alive
+        self._rows = 0
+
+    # ----------------------------------------------------------------- lifecycle
+    def close(self) -> None:
+        if getattr(self, "_h", None) is not None and self._h.value:
+            self._lib.gpuar_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        self.close()
+
+    def _stream(self) -> None:
+        s = torch.cuda.current_stream(self.device).cuda_stream
+        check(self._lib.gpuar_set_stream(self._h, ctypes.c_void_p(s)), "gpuar_set_stream")
+
+    # ----------------------------------------------------------------- state
+    @property
+    def epoch(self) -> int:
+        e = ctypes.c_uint32()
+        check(self._lib.gpuar_get_epoch(self._h, ctypes.byref(e)), "gpuar_get_epoch")
+        return int(e.value)
+
+    @epoch.setter
+    def epoch(self, e: int) -> None:
+        check(self._lib.gpuar_set_epoch(self._h, int(e) & 0xFFFFFFFF), "gpuar_set_epoch")
+
+    def set_selection_offset(self, s0: int) -> None:
+        check(self._lib.gpuar_set_selection_offset(self._h, int(s0)), "gpuar_set_selection_offset")
+
+    def set_max_trials(self, n: int) -> None:
+        check(self._lib.gpuar_set_max_trials(self._h, int(n)), "gpuar_set_max_trials")
+
+    @property
+    def path(self) -> str:
+        p = ctypes.c_int32()
+        check(self._lib.gpuar_path(self._h, ctypes.byref(p)), "gpuar_path")
+        return PATHS[p.value]
+
+    # ----------------------------------------------------------------- registration
+    def set_propensities(self, alpha: torch.Tensor) -> None:
+        """gpuar_set_propensities: (M,) shared vector or (rows, ld) row-major matrix."""
+        if alpha.device.type != "cuda" or alpha.dtype != torch.float32:
+            raise TypeError("alpha must be a float32 CUDA tensor")
+        if alpha.dim() == 1:
+            if alpha.numel() != self.M or not alpha.is_contiguous():
+                raise ValueError("shared vector must be contiguous with M elements")
+            rows, ld = 1, self.M
+        elif alpha.dim() == 2:
+            if alpha.stride(1) != 1:
+                raise ValueError("matrix rows must be contiguous")
+            rows, ld = alpha.shape[0], alpha.stride(0)
+            if alpha.shape[1] != self.M:
+                raise ValueError("matrix must have M columns (use a padded view for ld > M)")
+        else:
+            raise ValueError("alpha must be 1-D or 2-D")
+        with torch.cuda.device(self.device):
+            self._stream()
+            check(self._lib.gpuar_set_propensities(self._h, _ptr(alpha), rows, ld), "gpuar_set_propensities")
+        self._alpha = alpha
+        self._rows = rows
+
+    # ----------------------------------------------------------------- selection
+    def select(self, K: int | None = None, out: tuple | None = None, with_tau: bool = True,
+               with_trials: bool = True):
+        """gpuar_select -> (idx int32, tau float32, trials int32-view of uint32) CUDA tensors."""
+        K = (self._rows if self._rows > 1 else self.K) if K is None else int(K)
+        if out is None:
+            idx = torch.empty(K, dtype=torch.int32, device=self.device)
+            tau = torch.empty(K, dtype=torch.float32, device=self.device) if with_tau else None
+            trials = torch.empty(K, dtype=torch.int32, device=self.device) if with_trials else None
+        else:
+            idx, tau, trials = out
+        with torch.cuda.device(self.device):
+            self._stream()
+            check(self._lib.gpuar_select(self._h, K, _ptr(idx), _ptr(tau), _ptr(trials)), "gpuar_select")
+        return idx, tau, trials
+
+    def select_host(self, alpha: np.ndarray | torch.Tensor, K: int | None = None, out: tuple | None = None):
+        """gpuar_select_host: host (ideally pinned) propensities in, host outputs out."""
+        a = alpha if isinstance(alpha, torch.Tensor) else torch.from_numpy(np.ascontiguousarray(alpha, np.float32))
+        if a.dtype != torch.float32 or a.device.type != "cpu":
+            raise TypeError("alpha must be a float32 host array")
+        if a.dim() == 1:
+            rows, ld = 1, self.M
+        else:
+            rows, ld = a.shape[0], a.stride(0)
+        K = (rows if rows > 1 else self.K) if K is None else int(K)
+        if out is None:
+            pin = a.is_pinned()
+            idx = torch.empty(K, dtype=torch.int32, pin_memory=pin)
+            tau = torch.empty(K, dtype=torch.float32, pin_memory=pin)
+            trials = torch.empty(K, dtype=torch.int32, pin_memory=pin)
+        else:
+            idx, tau, trials = out
+        with torch.cuda.device(self.device):
+            self._stream()
+            check(self._lib.gpuar_select_host(self._h, _ptr(a), rows, ld, K, _ptr(idx), _ptr(tau), _ptr(trials)),
+                  "gpuar_select_host")
+        self._alpha = None
+        self._rows = 0
+        return idx, tau, trials
+
+    # ----------------------------------------------------------------- statistics / validation
+    def stats(self) -> tuple[float, float, float]:
+        amax, a0, p = ctypes.c_float(), ctypes.c_double(), ctypes.c_float()
+        with torch.cuda.device(self.device):
+            self._stream()
+            check(self._lib.gpuar_get_stats(self._h, ctypes.byref(amax), ctypes.byref(a0), ctypes.byref(p)),
+                  "gpuar_get_stats")
+        return float(amax.value), float(a0.value), float(p.value)
+
+    def row_stats(self) -> tuple[torch.Tensor, torch.Tensor]:
+        amax = torch.empty(self._rows, dtype=torch.float32, device=self.device)
+        a0 = torch.empty(self._rows, dtype=torch.float64, device=self.device)
+        with torch.cuda.device(self.device):
+            self._stream()
+            check(self._lib.gpuar_row_stats(self._h, _ptr(amax), _ptr(a0)), "gpuar_row_stats")
+        return amax, a0
+
+    def sync(self) -> None:
+        with torch.cuda.device(self.device):
+            self._stream()
+            check(self._lib.gpuar_sync(self._h), "gpuar_sync")
+
+    def histogram(self, idx: torch.Tensor, trials: torch.Tensor | None, hist: torch.Tensor | None = None,
+                  totals: torch.Tensor | None = None):
+        """gpuar_histogram: hist[M+1] (bin M = idx -1) and totals = (sum trials, #rejected), int64."""
+        if hist is None:
+            hist = torch.zeros(self.M + 1, dtype=torch.int64, device=self.device)
+        if totals is None:
+            totals = torch.zeros(2, dtype=torch.int64, device=self.device)
+        with torch.cuda.device(self.device):
+            self._stream()
+            check(self._lib.gpuar_histogram(self._h, _ptr(idx), _ptr(trials), idx.numel(), _ptr(hist), _ptr(totals)),
+                  "gpuar_histogram")
+        return hist, totals
+
+    def bench_philox(self, n_threads: int, calls: int, sink: torch.Tensor) -> None:
+        with torch.cuda.device(self.device):
+            self._stream()
+            check(self._lib.gpuar_bench_philox(self._h, int(n_threads), int(calls), _ptr(sink)), "gpuar_bench_philox")

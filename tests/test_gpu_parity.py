@@ -1,0 +1,329 @@
+"""GPU parity: libgpuar (through its C ABI via the thin binding) against the CPU oracle on
+the same seeded inputs.  idx and trials bit-exact; tau within 1e-6 relative of the
+oracle's binary64 tau_ref (north_star tolerance); per-row alpha_0 within 1e-6.
+"""
+import math
+
+import numpy as np
+import pytest
+import torch
+
+import oracle
+import synth
+
+pytestmark = pytest.mark.gpu
+
+SEED = synth.SELECT_SEED
+TAU_RTOL = 1e-6
+
+
+def _sel(M, K, seed=SEED):
+    from paper_1404_0027_b200 import Selector
+    return Selector(M, K, seed)
+
+
+def _check(gpu, ref, rows=None):
+    idx, tau, trials = (t.cpu().numpy() for t in gpu)
+    ridx, rtr = ref["idx"], ref["trials"]
+    sl = slice(None) if rows is None else rows
+    mism = np.nonzero(idx[sl] != ridx)[0]
+    assert mism.size == 0, f"{mism.size} idx mismatches, first at {mism[:5]}: gpu {idx[sl][mism[:5]]} oracle {ridx[mism[:5]]}"
+    np.testing.assert_array_equal(trials[sl].view(np.uint32), rtr)
+    tref = ref["tau_ref"]
+    g = tau[sl].astype(np.float64)
+    fin = np.isfinite(tref)
+    assert np.array_equal(np.isinf(g), np.isinf(tref)) and np.array_equal(np.isnan(g), np.isnan(tref))
+    rel = np.abs(g[fin] - tref[fin]) / tref[fin]
+    assert rel.size == 0 or rel.max() <= TAU_RTOL, rel.max()
+
+
+def _shared_case(alpha, K, epoch=0, s0=0, max_trials=None, seed=SEED):
+    a = np.asarray(alpha, np.float32)
+    sel = _sel(a.size, K, seed)
+    if max_trials:
+        sel.set_max_trials(max_trials)
+    sel.set_selection_offset(s0)
+    sel.epoch = epoch
+    sel.set_propensities(torch.from_numpy(a).cuda())
+    out = sel.select(K)
+    sel.sync()
+    ref = oracle.ar_select(a, K, seed=seed, epoch=epoch, s0=s0, max_trials=max_trials or (1 << 20), nthreads=8)
+    return sel, out, ref
+
+
+# ---------------------------------------------------------------- shared vector
+
+def test_c1_hand_1234_full():
+    sel, out, ref = _shared_case([1, 2, 3, 4], 10_000)
+    _check(out, ref)
+    amax, a0, p = sel.stats()
+    assert (amax, a0) == (4.0, 10.0) and abs(p - 0.625) < 1e-7
+    # chi-square against the exact law on the GPU's own outputs
+    h = np.bincount(out[0].cpu().numpy(), minlength=4)
+    assert oracle.chi2_pvalue(h, oracle.exact_law([1, 2, 3, 4]))[1] > 0.01
+
+
+@pytest.mark.parametrize("alpha", [[2, 1], [0, 5, 1], [3, 3, 3], [7.5]])
+def test_small_vectors(alpha):
+    _, out, ref = _shared_case(alpha, 4099)
+    _check(out, ref)
+
+
+def test_golden_file_values_on_gpu():
+    _, out, _ = _shared_case([1, 2, 3, 4], 8, seed=14040027)
+    assert out[0].cpu().tolist() == [2, 1, 3, 1, 3, 2, 2, 3]
+    assert out[2].cpu().tolist() == [1, 1, 1, 1, 1, 2, 2, 2]
+
+
+def test_c2_yeast_like_full():
+    sel, out, ref = _shared_case(synth.yeast_like(), 65536)
+    assert sel.path == "smem_f32"
+    _check(out, ref)
+    _, a0, _ = sel.stats()
+    assert abs(a0 - ref["a0"][0]) <= 1e-12 * a0
+
+
+@pytest.mark.parametrize("kind", ["uniform", "exponential", "pareto"])
+@pytest.mark.parametrize("M", [1000, 10_000, 100_000])
+def test_c3_distributions(kind, M):
+    a = synth.distribution(kind, M)
+    K = 1 << 14 if not (kind == "pareto" and M == 100_000) else 1 << 12
+    sel, out, ref = _shared_case(a, K)
+    assert sel.path == ("smem_f32" if M <= 50_000 else "smem_bf16_bracket")
+    _check(out, ref)
+    # acceptance rate vs a0/(M amax) within 4 sigma (north_star invariant)
+    p = oracle.acceptance_rate(a)
+    t = out[2].cpu().numpy().astype(np.float64)
+    assert abs(t.mean() - 1 / p) < 4 * math.sqrt((1 - p) / K) / p + 1e-9
+
+
+def test_group_max_path_pareto_1e6():
+    a = synth.pareto(1_000_000)
+    sel, out, ref = _shared_case(a, 256)
+    assert sel.path == "smem_group_max"
+    _check(out, ref)
+
+
+def test_group_max_path_uniform():
+    a = synth.uniform(600_000)
+    sel, out, ref = _shared_case(a, 20_000)
+    assert sel.path == "smem_group_max"
+    _check(out, ref)
+
+
+def test_bf16_bracket_boundaries():
+    # values exactly on / around bf16 grid points exercise every branch of the bracket
+    rng = np.random.default_rng(3)
+    base = rng.integers(0x3F000000, 0x40000000, size=70_000, dtype=np.uint32)
+    base[::3] &= 0xFFFF0000            # exactly representable in bf16
+    base[1::7] |= 0x0000FFFF           # just below the next bf16
+    a = base.view(np.float32).copy()
+    a[::11] = 0.0
+    sel, out, ref = _shared_case(a, 30_000)
+    assert sel.path == "smem_bf16_bracket"
+    _check(out, ref)
+
+
+def test_degenerate_and_single_nonzero():
+    _, out, ref = _shared_case([0, 0, 0, 0, 0], 1000)
+    _check(out, ref)
+    a = np.zeros(300, np.float32)
+    a[123] = 2.5
+    _, out, ref = _shared_case(a, 3000)
+    _check(out, ref)
+
+
+def test_invalid_vector_sticky_error():
+    from paper_1404_0027_b200 import GpuarError
+    sel = _sel(4, 64)
+    sel.set_propensities(torch.tensor([1.0, -1.0, 2.0, 3.0], device="cuda"))
+    idx, tau, trials = sel.select(64)
+    with pytest.raises(GpuarError) as e:
+        sel.sync()
+    assert e.value.status == -5
+    sel.sync()                                   # cleared after being reported
+    assert (idx.cpu() == -1).all() and torch.isnan(tau.cpu()).all()
+
+
+@pytest.mark.parametrize("mt", [1, 2, 3, 7])
+def test_max_trials_rejected_path(mt):
+    _, out, ref = _shared_case(synth.yeast_like(), 5000, max_trials=mt)
+    _check(out, ref)
+    assert (out[0].cpu() == -1).any()
+
+
+def test_epochs_offsets_and_replay():
+    a = synth.exponential(1000)
+    sel = _sel(a.size, 5000)
+    sel.set_propensities(torch.from_numpy(a).cuda())
+    first = [t.clone() for t in sel.select(5000)]
+    second = [t.clone() for t in sel.select(5000)]
+    assert sel.epoch == 2
+    assert not torch.equal(first[0], second[0])
+    sel.epoch = 0
+    again = sel.select(5000)
+    for x, y in zip(first, again):
+        assert torch.equal(x, y)
+    # sharding: two halves at offsets equal the whole
+    sel.epoch = 1
+    sel.set_selection_offset(0)
+    lo = [t.clone() for t in sel.select(2500)]
+    sel.epoch = 1
+    sel.set_selection_offset(2500)
+    hi = sel.select(2500)
+    for x, y, w in zip(lo, hi, second):
+        assert torch.equal(torch.cat([x, y]), w)
+    sel.sync()
+    _check(second, oracle.ar_select(a, 5000, seed=SEED, epoch=1, nthreads=8))
+
+
+def test_power_of_two_scaling_gpu():
+    a = synth.yeast_like()
+    _, base, _ = _shared_case(a, 20_000)
+    _, scaled, _ = _shared_case(a * np.float32(2.0**-40), 20_000)
+    assert torch.equal(base[0], scaled[0]) and torch.equal(base[2], scaled[2])
+    assert torch.equal(scaled[1], base[1] * 2.0**40)
+
+
+# ---------------------------------------------------------------- per-realization rows
+
+def _rows_case(M, K, ld=None, k0=0, epoch=0, max_trials=None, rates=None, mutate=None):
+    rates = synth.yeast_rates(M) if rates is None else rates
+    host = synth.rows(rates, synth.GEN_SEED, k0, K, ld=ld)
+    if mutate:
+        mutate(host)
+    sel = _sel(M, K)
+    if max_trials:
+        sel.set_max_trials(max_trials)
+    sel.set_selection_offset(k0)
+    sel.epoch = epoch
+    dev = torch.from_numpy(host).cuda()
+    view = dev[:, :M] if ld else dev
+    sel.set_propensities(view)
+    assert sel.path == "rows"
+    out = sel.select(K)
+    amax, a0 = sel.row_stats()
+    ref = oracle.ar_select(host, K, seed=SEED, epoch=epoch, s0=k0, M=M,
+                           max_trials=max_trials or (1 << 20), nthreads=8)
+    return sel, out, ref, (amax, a0)
+
+
+@pytest.mark.parametrize("M,K", [(1029, 4096), (1029, 1000), (1, 100), (2, 333), (3, 257), (5, 64),
+                                 (255, 1111), (256, 512), (257, 300), (4096, 200), (7000, 64)])
+def test_rows_parity(M, K):
+    sel, out, ref, (amax, a0) = _rows_case(M, K)
+    sel.sync()
+    _check(out, ref)
+    np.testing.assert_array_equal(amax.cpu().numpy(), ref["amax"])
+    d = a0.cpu().numpy()
+    np.testing.assert_allclose(d, ref["a0"], rtol=1e-6)
+
+
+def test_rows_padded_pitch_and_offset():
+    sel, out, ref, _ = _rows_case(1029, 999, ld=1036, k0=12345, epoch=5)
+    _check(out, ref)
+
+
+def test_rows_invalid_and_zero_rows():
+    from paper_1404_0027_b200 import GpuarError
+
+    def mutate(h):
+        h[3, :] = 0.0
+        h[10, 7] = np.float32(-1.0)
+        h[11, 8] = np.nan
+    sel, out, ref, _ = _rows_case(1029, 64, mutate=mutate)
+    with pytest.raises(GpuarError):
+        sel.sync()
+    _check(out, ref)
+
+
+def test_rows_max_trials():
+    sel, out, ref, _ = _rows_case(1029, 2000, max_trials=33)
+    _check(out, ref)
+
+
+@pytest.mark.slow
+def test_c4_full_size_sampled():
+    """c4 at its full size (K = 2^20, M = 1029, generated in HBM by libsynth), in the
+    launch configuration bench.py times; oracle on sampled rows: the first and last 4096
+    and every 997th."""
+    import synth.gpu as sg
+    from paper_1404_0027_b200 import Selector
+    M, K = synth.YEAST_M, 1 << 20
+    rates = synth.yeast_rates(M)
+    d_rates = torch.from_numpy(rates).cuda()
+    mat = torch.empty((K, M), dtype=torch.float32, device="cuda")
+    sg.fill_rows(mat, d_rates, synth.GEN_SEED, 0)
+    sel = Selector(M, K, SEED)
+    sel.set_propensities(mat)
+    idx, tau, trials = sel.select(K)
+    sel.sync()
+    rows = np.unique(np.concatenate([np.arange(4096), np.arange(K - 4096, K), np.arange(0, K, 997)]))
+    # check the generator agrees on the sampled rows, then run the oracle on host rows
+    host = np.concatenate([synth.rows(rates, synth.GEN_SEED, int(r), 1) for r in rows[:64]])
+    np.testing.assert_array_equal(mat[torch.from_numpy(rows[:64]).cuda()].cpu().numpy(), host)
+    gi, gt, gtr = idx.cpu().numpy(), tau.cpu().numpy(), trials.cpu().numpy().view(np.uint32)
+    for start in range(0, rows.size, 4096):
+        rr = rows[start:start + 4096]
+        # contiguous runs: oracle per run
+        splits = np.nonzero(np.diff(rr) != 1)[0] + 1
+        for run in np.split(rr, splits):
+            h = synth.rows(rates, synth.GEN_SEED, int(run[0]), run.size)
+            ref = oracle.ar_select(h, run.size, seed=SEED, s0=int(run[0]), nthreads=8)
+            np.testing.assert_array_equal(gi[run], ref["idx"])
+            np.testing.assert_array_equal(gtr[run], ref["trials"])
+            fin = np.isfinite(ref["tau_ref"])
+            rel = np.abs(gt[run][fin] - ref["tau_ref"][fin]) / ref["tau_ref"][fin]
+            assert rel.max() <= TAU_RTOL
+    # properties at every row: trials >= 1, chosen reaction enabled
+    assert (gtr >= 1).all() and (gi >= 0).all()
+    chosen = mat[torch.arange(K, device="cuda"), idx.long()]
+    assert (chosen > 0).all()
+
+
+# ---------------------------------------------------------------- host path, helpers
+
+def test_select_host_matches_device_rows():
+    from paper_1404_0027_b200 import Selector
+    M, K = 1029, 20_000
+    host = torch.from_numpy(synth.rows(synth.yeast_rates(M), synth.GEN_SEED, 0, K)).pin_memory()
+    sel = Selector(M, K, SEED)
+    hi, ht, htr = sel.select_host(host)
+    sel.epoch = 0
+    sel.set_propensities(host.cuda())
+    di, dt, dtr = sel.select(K)
+    assert torch.equal(hi, di.cpu()) and torch.equal(ht, dt.cpu()) and torch.equal(htr, dtr.cpu())
+
+
+def test_select_host_shared_vector():
+    from paper_1404_0027_b200 import Selector
+    a = synth.yeast_like()
+    sel = Selector(a.size, 30_000, SEED)
+    hi, ht, htr = sel.select_host(torch.from_numpy(a).pin_memory(), K=30_000)
+    ref = oracle.ar_select(a, 30_000, seed=SEED, nthreads=8)
+    _check((hi, ht, htr), ref)
+
+
+def test_histogram_kernel():
+    a = synth.yeast_like()
+    sel, out, ref = _shared_case(a, 65536, max_trials=64)
+    hist, totals = sel.histogram(out[0], out[2])
+    h, ts = oracle.histogram(ref["idx"], ref["trials"], a.size)
+    np.testing.assert_array_equal(hist.cpu().numpy(), h.astype(np.int64))
+    assert totals[0].item() == ts and totals[1].item() == h[-1]
+
+
+def test_synth_gpu_rows_match_numpy():
+    import synth.gpu as sg
+    rates = synth.yeast_rates()
+    out = torch.empty((300, 1032), dtype=torch.float32, device="cuda")
+    sg.fill_rows(out, torch.from_numpy(rates).cuda(), 99, 777)
+    np.testing.assert_array_equal(out.cpu().numpy(), synth.rows(rates, 99, 777, 300, ld=1032))
+
+
+def test_bench_philox_runs():
+    sel = _sel(4, 4)
+    sink = torch.zeros(1024, dtype=torch.int32, device="cuda")
+    sel.bench_philox(1024, 8, sink)
+    sel.sync()
+    assert sink.abs().sum().item() > 0
