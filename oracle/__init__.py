@@ -75,6 +75,11 @@ def _load():
             ctypes.c_void_p, ctypes.c_int64, ctypes.c_int64, ctypes.c_int64, ctypes.c_int64,
             ctypes.c_uint64, ctypes.c_uint32, ctypes.c_uint32, ctypes.c_void_p, ctypes.c_int]
         lib.oracle_it_batch.restype = ctypes.c_int
+        lib.oracle_argmin_batch.argtypes = [
+            ctypes.c_void_p, ctypes.c_int64, ctypes.c_int64, ctypes.c_int64, ctypes.c_int64, ctypes.c_float,
+            ctypes.c_uint64, ctypes.c_uint32, ctypes.c_uint32, ctypes.c_void_p, ctypes.c_void_p,
+            ctypes.c_void_p, ctypes.c_int]
+        lib.oracle_argmin_batch.restype = ctypes.c_int
         lib.oracle_histogram.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int64,
                                          ctypes.c_int64, ctypes.c_void_p, ctypes.c_void_p]
         lib.oracle_histogram.restype = None
@@ -181,6 +186,52 @@ def it_select(alpha, K: int, seed: int, epoch: int = 0, s0: int = 0,
     idx = np.empty(K, np.int32)
     _load().oracle_it_batch(_ptr(a), M, rows, ld, K, seed & (2**64 - 1), s0, epoch, _ptr(idx), nthreads)
     return idx
+
+
+def argmin_select(alpha, K: int, seed: int, w: float = 1.0, epoch: int = 0, s0: int = 0,
+                  M: int | None = None, nthreads: int = 1) -> dict:
+    """The paper's printed GPU/AR rule (election + argmin selection, PAPER.md:304-380,
+    498-560) on Philox stream tag 3, threshold T = fl32(w * alpha_max).  Returns idx (int32,
+    -1 = rejected/degenerate), tau, tau_ref and the status."""
+    a = _f32(alpha)
+    if a.ndim == 1:
+        rows, ld = 1, a.shape[0]
+    else:
+        rows, ld = a.shape[0], a.shape[1]
+        if rows != K:
+            raise ValueError("matrix rows must equal K")
+    M = ld if M is None else M
+    idx = np.empty(K, np.int32)
+    tau = np.empty(K, np.float32)
+    tau_ref = np.empty(K, np.float64)
+    st = _load().oracle_argmin_batch(_ptr(a), M, rows, ld, K, float(w), seed & (2**64 - 1), s0, epoch,
+                                     _ptr(idx), _ptr(tau), _ptr(tau_ref), nthreads)
+    return dict(idx=idx, tau=tau, tau_ref=tau_ref, status=int(st))
+
+
+def argmin_law(alpha, w: float = 1.0, reject: bool = False):
+    """Exact law of the argmin rule with continuous uniforms:
+    P(j) = int_0^1 (D_j/T) prod_{i != j} (1 - r D_i/T) dr,  T = w max D.
+    The integrand is a polynomial of degree M-1 in r, so Gauss-Legendre with ceil(M/2)+1
+    nodes is exact.  With reject=True also returns P(rejected) = prod_i (1 - D_i/T)."""
+    d = np.asarray(alpha, np.float64) / (w * float(np.max(alpha)))
+    M = d.size
+    x, wts = np.polynomial.legendre.leggauss(M // 2 + 2)
+    r = 0.5 * (x + 1.0)
+    wts = 0.5 * wts
+    one_minus = 1.0 - np.outer(r, d)                      # (nodes, M)
+    with np.errstate(divide="ignore"):
+        logs = np.log(np.abs(one_minus))
+    zero = one_minus == 0.0
+    # prod over i != j: exp(sum log - log_j), handling exact zeros (d_i = 1 at r = 1 only)
+    total = logs.sum(axis=1, keepdims=True)
+    prod_except = np.exp(total - logs)
+    nz = zero.sum(axis=1, keepdims=True)
+    prod_except = np.where(nz == 0, prod_except, 0.0)
+    P = (d[None, :] * prod_except * wts[:, None]).sum(axis=0)
+    if reject:
+        return P, float(np.prod(1.0 - d))
+    return P
 
 
 def histogram(idx, trials, M: int) -> tuple[np.ndarray, int]:

@@ -40,6 +40,7 @@
  *   tag 0: AR trials, call = i >> 1, trial i uses words (x0,x1) if i even, (x2,x3) if odd
  *   tag 1: tau uniform u1 (call 0, word x0)
  *   tag 2: IT uniform u2  (call 0, word x0)
+ *   tag 3: election draws of the paper's argmin rule (call j >> 2, word j & 3)
  */
 #include <float.h>
 #include <math.h>
@@ -279,6 +280,82 @@ int oracle_it_batch(const float *alpha, int64_t M, int64_t rows, int64_t ld, int
         uint32_t x[4];
         draw(seed, 0u, s0 + (uint32_t)r, epoch, 2u, x);
         idx[r] = oracle_it_one(row, M, a0, oracle_unit(x[0]));
+    }
+    return status;
+}
+
+/* ------------------------------------------------------------------ the paper's printed rule (NEXT-1) */
+
+/* Election + selection of PAPER.md:304-380 / pseudo-code PAPER.md:498-560 ("argmin rule"),
+ * with the readings of DESIGN.md R16-R19:
+ *   threshold T = fl32(w * alpha_max)  (T_w of PAPER.md:566-568);
+ *   election: for every reaction j draw v_j = (x>>8) 2^-24 in [0,1)
+ *     from Philox ctr {j >> 2, s, epoch, 3}, word j & 3; u_j = fl32(v_j * T);
+ *     eligible iff u_j < D_j (then D_j > 0), rated R_j = fl32(u_j / D_j);
+ *     not eligible: R_j = 1.0 (sentinel; the pseudo-code's T*10 is a bug);
+ *   selection: j* = argmin_j R_j, ties to the lowest j;
+ *     if R_j* >= 1 the election failed: rejected (idx -1; the paper's M+1).
+ * trials = M (draws consumed). tau as for the classic rule. */
+void oracle_argmin_one(const float *alpha, int64_t M, float amax, double a0, float w,
+                       uint64_t seed, uint32_t s, uint32_t epoch,
+                       int32_t *idx, float *tau, double *tau_ref)
+{
+    if (amax == 0.0f) {
+        *idx = -1;
+        *tau = INFINITY;
+        *tau_ref = INFINITY;
+        return;
+    }
+    float T = w * amax;
+    float best = 1.0f;
+    int32_t best_j = -1;
+    uint32_t x[4];
+    for (int64_t j = 0; j < M; ++j) {
+        if ((j & 3) == 0) draw(seed, (uint32_t)(j >> 2), s, epoch, 3u, x);
+        float v = oracle_unit(x[j & 3]);
+        float u = v * T;
+        float R = 1.0f;
+        if (u < alpha[j]) R = u / alpha[j];
+        if (R < best) {           /* strict: ties keep the lowest index */
+            best = R;
+            best_j = (int32_t)j;
+        }
+    }
+    *idx = best_j;                /* -1 when every rating is >= 1 */
+    uint32_t t[4];
+    draw(seed, 0u, s, epoch, 1u, t);
+    float u1 = oracle_unit_open(t[0]);
+    *tau = -logf(u1) / (float)a0;
+    *tau_ref = -log((double)u1) / a0;
+}
+
+int oracle_argmin_batch(const float *alpha, int64_t M, int64_t rows, int64_t ld, int64_t K, float w,
+                        uint64_t seed, uint32_t s0, uint32_t epoch,
+                        int32_t *idx, float *tau, double *tau_ref, int nthreads)
+{
+    int status = ORACLE_OK;
+    float shared_amax = 0.0f;
+    double shared_a0 = 0.0;
+    if (rows == 1 && oracle_stats(alpha, M, &shared_amax, &shared_a0) != ORACLE_OK)
+        status = ORACLE_EPROPENSITY;
+#pragma omp parallel for schedule(dynamic, 64) num_threads(nthreads > 0 ? nthreads : 1)
+    for (int64_t r = 0; r < K; ++r) {
+        const float *row = (rows == 1) ? alpha : alpha + r * ld;
+        float amax = shared_amax;
+        double a0 = shared_a0;
+        int ok = (rows == 1) ? (status == ORACLE_OK)
+                             : (oracle_stats(row, M, &amax, &a0) == ORACLE_OK);
+        if (!ok) {
+            idx[r] = -1;
+            tau[r] = NAN;
+            tau_ref[r] = NAN;
+            if (rows != 1) {
+#pragma omp atomic write
+                status = ORACLE_EPROPENSITY;
+            }
+            continue;
+        }
+        oracle_argmin_one(row, M, amax, a0, w, seed, s0 + (uint32_t)r, epoch, &idx[r], &tau[r], &tau_ref[r]);
     }
     return status;
 }

@@ -15,7 +15,8 @@ using namespace gpuar;
 
 namespace {
 
-constexpr int kRowsMaxWarps = 16;
+constexpr int kRowsMaxWarps = 32;      // compiled variants: <=16, <=24, <=32 warps per CTA
+constexpr int kRowsDefaultWarps = 24;   // r01 sweep: 24 warps x 2 slots -> 5.92 TB/s (16x3: 5.13)
 constexpr size_t kHostChunkBytes = 64ull << 20;  // gpuar_select_host row-chunk size
 
 struct Chunked {
@@ -130,7 +131,7 @@ void plan_shared(gpuar_handle* h) {
 int plan_rows(gpuar_handle* h) {
   const uint64_t budget = (uint64_t)h->smem_optin - 1024u;
   const uint64_t sb = ((4ull * (uint64_t)h->M + 15ull) & ~15ull) + 16ull;
-  int W = env_int("GPUAR_ROWS_WARPS", kRowsMaxWarps);
+  int W = env_int("GPUAR_ROWS_WARPS", kRowsDefaultWarps);
   W = std::max(1, std::min(W, kRowsMaxWarps));
   int S = env_int("GPUAR_ROWS_STAGES", 0);
   auto fits = [&](int w, int s) { return (((uint64_t)w * s * 8u + 127u) & ~127ull) + (uint64_t)w * s * sb <= budget; };
@@ -138,6 +139,7 @@ int plan_rows(gpuar_handle* h) {
     S = 4;
     while (S > 2 && !fits(W, S)) --S;
   }
+  if (S > 1 && !fits(W, S) && W > 16) S = 1;   // many warps with no prefetch beat few with it
   while (W > 1 && !fits(W, S)) --W;
   if (!fits(W, S) || S > 32) return GPUAR_EINVAL;  // M too large for the row pipeline
   h->rows_warps = W;

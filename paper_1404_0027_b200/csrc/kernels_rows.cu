@@ -26,9 +26,35 @@ namespace gpuar {
 
 namespace {
 
-constexpr uint32_t kMaxWarps = 16;
+// Trials of one row by one warp: round t = Philox calls [32t, 32t+32), lane l -> call
+// 32t + l -> trials 2c, 2c+1; the ballot's lowest lane (even trial first) is the first
+// accept in canonical order (R6).
+template <bool FOLD>
+__device__ __forceinline__ void row_trials(const TrialStream& ts, uint32_t sel, uint32_t row_s, uint32_t M,
+                                           float amax, uint32_t half, uint32_t calls, uint32_t lane, int32_t& id,
+                                           uint32_t& tr) {
+  const float amax_s = __fmul_rn(amax, 0x1p-24f);
+  for (uint32_t c0 = 0; c0 < calls; c0 += 32u) {
+    const uint32_t c = c0 + lane;
+    const Philox4 x = ts(c, sel);
+    const uint32_t j0 = __umulhi(x.x, M);
+    const uint32_t j1 = __umulhi(x.z, M);
+    const float v0 = lds_f32(row_s + 4u * j0);
+    const float v1 = lds_f32(row_s + 4u * j1);
+    const bool a0 = (c < calls) & (scaled_u<FOLD>(x.y, amax, amax_s) < v0);
+    const bool a1 = (c < half) & (scaled_u<FOLD>(x.w, amax, amax_s) < v1);
+    const uint32_t b = __ballot_sync(kFull, a0 || a1);
+    if (b != 0u) {
+      const uint32_t w = __ffs(b) - 1;
+      id = (int32_t)__shfl_sync(kFull, a0 ? j0 : j1, w);
+      tr = __shfl_sync(kFull, a0 ? 2u * c + 1u : 2u * c + 2u, w);
+      return;
+    }
+  }
+}
 
-__global__ void __launch_bounds__(kMaxWarps * 32, 1) select_rows_kernel(const RowsParams P) {
+template <int MAXW>
+__global__ void __launch_bounds__(MAXW * 32, 1) select_rows_kernel(const RowsParams P) {
   extern __shared__ __align__(128) unsigned char smem[];
   const uint32_t warps = blockDim.x >> 5;
   const uint32_t warp = threadIdx.x >> 5;
@@ -65,6 +91,7 @@ __global__ void __launch_bounds__(kMaxWarps * 32, 1) select_rows_kernel(const Ro
 
   const uint32_t half = P.max_trials >> 1;
   const uint32_t calls = half + (P.max_trials & 1u);
+  const TrialStream ts(P.seed_lo, P.seed_hi, P.epoch);
   const uint32_t full_chunks = M >> 8;  // 256 elements = 8 per lane
   float nlog = 0.f;                     // -ln(u1) of row_of(n0 + lane)
 
@@ -81,14 +108,15 @@ __global__ void __launch_bounds__(kMaxWarps * 32, 1) select_rows_kernel(const Ro
     const float* row = reinterpret_cast<const float*>(ring + (size_t)slot * SB + ((r * row_bytes) & 15ull));
 
     // ---- alpha_max (max of bit patterns) and alpha_0
+    const uint32_t row_s = smem_u32(row);
     uint32_t mx = 0;
     double acc = 0.0;
     for (uint32_t ch = 0; ch < full_chunks; ++ch) {
-      const float* p = row + ch * 256u + lane;
+      const uint32_t p = row_s + 4u * (ch * 256u + lane);
       float v[8];
 #pragma unroll
       for (int k = 0; k < 8; ++k) {
-        v[k] = p[k * 32];
+        v[k] = lds_f32(p + 128u * k);
         mx = max(mx, __float_as_uint(v[k]));
       }
       const float s = __fadd_rn(__fadd_rn(__fadd_rn(v[0], v[1]), __fadd_rn(v[2], v[3])),
@@ -98,7 +126,7 @@ __global__ void __launch_bounds__(kMaxWarps * 32, 1) select_rows_kernel(const Ro
     {
       float s = 0.f;  // tail: at most 8 elements per lane, sequential
       for (uint32_t j = (full_chunks << 8) + lane; j < M; j += 32u) {
-        const float v = row[j];
+        const float v = lds_f32(row_s + 4u * j);
         mx = max(mx, __float_as_uint(v));
         s = __fadd_rn(s, v);
       }
@@ -126,23 +154,12 @@ __global__ void __launch_bounds__(kMaxWarps * 32, 1) select_rows_kernel(const Ro
       } else {
         const float amax = __uint_as_float(mx);
         tau = __fdiv_rn(nl, __double2float_rn(acc));
-        tr = P.max_trials;
-        const uint32_t sg = P.s0 + (uint32_t)r;
-        for (uint32_t c0 = 0; c0 < calls; c0 += 32u) {
-          const uint32_t c = c0 + lane;
-          const Philox4 x = philox4x32_10(c, sg, P.epoch, kTagTrials, P.seed_lo, P.seed_hi);
-          const uint32_t j0 = __umulhi(x.x, M);
-          const uint32_t j1 = __umulhi(x.z, M);
-          const bool a0 = c < calls && __fmul_rn(unit24(x.y), amax) < row[j0];
-          const bool a1 = !a0 && c < half && __fmul_rn(unit24(x.w), amax) < row[j1];
-          const uint32_t b = __ballot_sync(kFull, a0 || a1);
-          if (b != 0u) {
-            const uint32_t w = __ffs(b) - 1;
-            id = (int32_t)__shfl_sync(kFull, a0 ? j0 : j1, w);
-            tr = __shfl_sync(kFull, a0 ? 2u * c + 1u : 2u * c + 2u, w);
-            break;
-          }
-        }
+        const uint32_t sel = ts.sel_word(P.s0 + (uint32_t)r);
+        if (can_fold(mx))
+          row_trials<true>(ts, sel, row_s, M, amax, half, calls, lane, id, tr);
+        else
+          row_trials<false>(ts, sel, row_s, M, amax, half, calls, lane, id, tr);
+        if (id < 0) tr = P.max_trials;
       }
       if (lane == 0) {
         P.idx[r] = id;
@@ -162,18 +179,31 @@ __global__ void __launch_bounds__(kMaxWarps * 32, 1) select_rows_kernel(const Ro
 
 cudaError_t launch_select_rows(const RowsParams& p, int grid, int warps, cudaStream_t st) {
   const size_t sh = (((size_t)warps * p.stages * 8u + 127u) & ~(size_t)127u) + (size_t)warps * p.stages * p.stage_bytes;
-  select_rows_kernel<<<grid, warps * 32, sh, st>>>(p);
+  if (warps <= 16)
+    select_rows_kernel<16><<<grid, warps * 32, sh, st>>>(p);
+  else if (warps <= 24)
+    select_rows_kernel<24><<<grid, warps * 32, sh, st>>>(p);
+  else
+    select_rows_kernel<32><<<grid, warps * 32, sh, st>>>(p);
   return cudaGetLastError();
 }
 
 int select_rows_blocks_per_sm(int warps, size_t smem) {
   int n = 0;
-  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, select_rows_kernel, warps * 32, smem) != cudaSuccess) return 0;
-  return n;
+  cudaError_t e;
+  if (warps <= 16)
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, select_rows_kernel<16>, warps * 32, smem);
+  else if (warps <= 24)
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, select_rows_kernel<24>, warps * 32, smem);
+  else
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, select_rows_kernel<32>, warps * 32, smem);
+  return e == cudaSuccess ? n : 0;
 }
 
 void set_select_rows_limits(int bytes) {
-  cudaFuncSetAttribute(select_rows_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+  cudaFuncSetAttribute(select_rows_kernel<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+  cudaFuncSetAttribute(select_rows_kernel<24>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+  cudaFuncSetAttribute(select_rows_kernel<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
 }
 
 }  // namespace gpuar

@@ -23,26 +23,173 @@ namespace gpuar {
 
 namespace {
 
+// Exact acceptance test fl32(u*amax) < alpha_j on the shared-memory copy (path 1) or with
+// an exact prefilter (paths 2, 3).  `sbase` is the shared-state-space address of the
+// staged array (32-bit; no generic->shared conversion per gather).
 template <int PATH>
-__device__ __forceinline__ bool accept(float t, uint32_t j, const void* sm, const float* __restrict__ alpha,
+__device__ __forceinline__ bool accept(float t, uint32_t j, uint32_t sbase, const float* __restrict__ alpha,
                                        uint32_t group_shift) {
   if constexpr (PATH == kPathSmemF32) {
-    return t < static_cast<const float*>(sm)[j];
+    return t < lds_f32(sbase + 4u * j);
   } else if constexpr (PATH == kPathSmemBf16) {
     // bf16(code) <= alpha_j < bf16(code + 1): decide without the exact value unless t
-    // falls inside that bracket (exact: DESIGN.md "prefilter").
-    const uint32_t code = static_cast<const uint16_t*>(sm)[j];
-    const float lo = __uint_as_float(code << 16);
-    const float hi = __uint_as_float((code + 1u) << 16);
-    if (t < lo) return true;
-    if (t >= hi) return false;
+    // falls inside that bracket (exact: DESIGN.md §5.2).
+    const uint32_t code = lds_u16(sbase + 2u * j);
+    const bool lo = t < __uint_as_float(code << 16);
+    const bool hi = t >= __uint_as_float((code + 1u) << 16);
+    if (lo | hi) return lo;
     return t < __ldg(alpha + j);
   } else {
     // group maximum rounded up to bf16 is an upper bound of alpha_j
-    const float ub = __uint_as_float(static_cast<uint32_t>(static_cast<const uint16_t*>(sm)[j >> group_shift]) << 16);
-    if (t >= ub) return false;
+    if (t >= __uint_as_float(lds_u16(sbase + 2u * (j >> group_shift)) << 16)) return false;
     return t < __ldg(alpha + j);
   }
+}
+
+struct Pool {
+  unsigned long long next, end, grab, base_next;
+  bool exhausted;
+};
+
+// Hand idle teams (leader lanes in `need`) the next selections of the warp's pool,
+// refilling it with one atomic per `grab` selections.  Returns the new selection of this
+// lane's team (broadcast from its leader) or kNone.
+__device__ __forceinline__ uint32_t pool_take(Pool& pl, uint32_t need, uint32_t lane, uint32_t tbase, uint32_t K,
+                                              DevCounters* ctr) {
+  uint32_t got = kNone;
+  while (need != 0u && !pl.exhausted) {
+    if (pl.next >= pl.end) {
+      unsigned long long b = 0;
+      if (lane == 0u) b = pl.base_next + atomicAdd(&ctr->next, pl.grab);
+      b = __shfl_sync(kFull, b, 0);
+      if (b >= K) {
+        pl.exhausted = true;
+        break;
+      }
+      pl.next = b;
+      pl.end = min(b + pl.grab, (unsigned long long)K);
+    }
+    const uint32_t avail = (uint32_t)(pl.end - pl.next);
+    const uint32_t r = __popc(need & lanemask_lt());
+    uint32_t mine = kNone;
+    if (((need >> lane) & 1u) && r < avail) mine = (uint32_t)pl.next + r;
+    mine = __shfl_sync(kFull, mine, tbase);
+    if (mine != kNone) got = mine;
+    const uint32_t taken = min((uint32_t)__popc(need), avail);
+    pl.next += taken;
+    // leaders that got work drop out of `need`
+    const uint32_t served = __ballot_sync(kFull, ((need >> lane) & 1u) && r < avail);
+    need &= ~served;
+  }
+  return got;
+}
+
+// Trial phase of one warp.  g = lanes per team (power of two); TEAM = (g > 1).
+// Fast path: one Philox call + two gathers + one vote per round; team bookkeeping only
+// when some lane of the warp finished a selection.
+template <int PATH, bool FOLD, bool TEAM>
+__device__ __forceinline__ void trial_loop(const SharedParams& P, const TrialStream& ts, uint32_t sbase, float amax,
+                                           uint32_t g, Pool pl) {
+  const float amax_s = __fmul_rn(amax, 0x1p-24f);
+  const uint32_t M = P.M, K = P.K;
+  const uint32_t half = P.max_trials >> 1;            // calls whose odd trial is < max_trials
+  const uint32_t calls = half + (P.max_trials & 1u);  // calls whose even trial is < max_trials
+  const uint32_t lane = threadIdx.x & 31u;
+  const uint32_t tbase = lane & ~(g - 1u);
+  const uint32_t rank = lane & (g - 1u);
+  const uint32_t tmask = (g == 32u) ? kFull : (((1u << g) - 1u) << tbase);
+  const bool leader = rank == 0u;
+
+  uint32_t my = kNone;  // local selection of this lane's team
+  uint32_t sel = 0;     // its round-1 Philox word
+  uint32_t c = 0;       // this lane's Philox call within the selection
+
+  while (true) {
+    const uint32_t need = __ballot_sync(kFull, leader && my == kNone);
+    if (need != 0u) {
+      const uint32_t got = pool_take(pl, need, lane, tbase, K, P.ctr);
+      if (got != kNone) {
+        my = got;
+        sel = ts.sel_word(P.s0 + got);
+        c = rank;
+      }
+    }
+    if (pl.exhausted && __all_sync(kFull, my == kNone)) break;
+    const bool active = my != kNone;
+
+    bool a0, a1, out;
+    uint32_t j0, j1, ball;
+    while (true) {
+      const Philox4 x = ts(c, sel);
+      j0 = __umulhi(x.x, M);
+      j1 = __umulhi(x.z, M);
+      const float t0 = scaled_u<FOLD>(x.y, amax, amax_s);
+      const float t1 = scaled_u<FOLD>(x.w, amax, amax_s);
+      // branch-free: both gathers always issue (j < M is always a valid index)
+      const bool r0 = accept<PATH>(t0, j0, sbase, P.alpha, P.group_shift);
+      const bool r1 = accept<PATH>(t1, j1, sbase, P.alpha, P.group_shift);
+      a0 = active & (c < calls) & r0;
+      a1 = active & (c < half) & r1;
+      if constexpr (TEAM) {
+        ball = __ballot_sync(kFull, a0 || a1);
+        out = active && c - rank + g >= calls;   // the team's next round would start past max_trials
+        if (ball != 0u || __any_sync(kFull, out)) break;
+        c += g;
+      } else {
+        out = active && c + 1u >= calls;
+        if (__any_sync(kFull, a0 || a1 || out)) break;
+        ++c;
+      }
+    }
+    // slow path: resolve finished selections
+    if constexpr (TEAM) {
+      const uint32_t b = ball & tmask;
+      uint32_t wj = 0, wt = 0;
+      if (ball != 0u) {
+        const uint32_t src = b ? (uint32_t)(__ffs(b) - 1) : lane;
+        wj = __shfl_sync(kFull, a0 ? j0 : j1, src);
+        wt = __shfl_sync(kFull, a0 ? 2u * c + 1u : 2u * c + 2u, src);
+      }
+      if (active) {
+        if (b != 0u || out) {
+          if (leader) {
+            P.idx[my] = b ? (int32_t)wj : -1;
+            if (P.trials) P.trials[my] = b ? wt : P.max_trials;
+          }
+          my = kNone;
+        } else {
+          c += g;
+        }
+      }
+    } else {
+      if (active) {
+        if (a0 || a1 || out) {
+          P.idx[my] = a0 ? (int32_t)j0 : (a1 ? (int32_t)j1 : -1);
+          if (P.trials) P.trials[my] = a0 ? 2u * c + 1u : (a1 ? 2u * c + 2u : P.max_trials);
+          my = kNone;
+        } else {
+          ++c;
+        }
+      }
+    }
+  }
+}
+
+// Team size g (power of two, 1..32): minimise (waste in the last round ~ g p) +
+// (idle lanes while a warp's last selections drain ~ T ln T * warps / K, T = 32/g teams).
+__device__ __forceinline__ uint32_t choose_team(float p, uint32_t K, uint32_t nwarps) {
+  const float wk = (float)nwarps / (float)max(K, 1u);
+  uint32_t best = 1u;
+  float best_cost = 3.0e38f;
+  for (uint32_t g = 1u; g <= 32u; g <<= 1) {
+    const float T = (float)(32u / g);
+    const float cost = (float)g * p + T * __logf(T + 1.0f) * wk;
+    if (cost < best_cost) {
+      best_cost = cost;
+      best = g;
+    }
+  }
+  return best;
 }
 
 template <int PATH>
@@ -72,91 +219,41 @@ __global__ void __launch_bounds__(1024, 1) select_shared_kernel(const SharedPara
     for (uint32_t j = threadIdx.x; j < P.M; j += blockDim.x) sv[j] = __ldg(P.alpha + j);
   } else {
     uint16_t* pf = reinterpret_cast<uint16_t*>(smem);
-    for (uint32_t g = threadIdx.x; g < P.n_pref; g += blockDim.x) pf[g] = __ldg(P.prefilter + g);
+    for (uint32_t i = threadIdx.x; i < P.n_pref; i += blockDim.x) pf[i] = __ldg(P.prefilter + i);
   }
   __syncthreads();
+  const uint32_t sbase = smem_u32(smem);
 
   // ---- phase C: trials
   const float amax = __uint_as_float(st.amax_bits);
-  const uint32_t M = P.M, K = P.K;
-  const uint32_t half = P.max_trials >> 1;                 // calls whose odd trial is < max_trials
-  const uint32_t calls = half + (P.max_trials & 1u);       // calls whose even trial is < max_trials
-  // team size: enough teams to cover K, and g*p <= ~1/4 so the last round wastes little
-  uint32_t g = 32u;
-  {
-    const uint32_t ratio = max(1u, nthreads / max(K, 1u));
-    g = min(g, 1u << (31 - __clz(ratio)));
-    const float lim = st.p > 0.f ? 0.25f / st.p : 32.f;
-    const uint32_t gl = lim >= 32.f ? 32u : (lim < 1.f ? 1u : (uint32_t)lim);
-    g = min(g, 1u << (31 - __clz(gl)));
-  }
-  const uint32_t lane = threadIdx.x & 31u;
-  const uint32_t tbase = lane & ~(g - 1u);
-  const uint32_t rank = lane & (g - 1u);
-  const uint32_t tmask = (g == 32u) ? kFull : (((1u << g) - 1u) << tbase);
-  const bool leader = rank == 0u;
-  const unsigned long long grab = st.grab;
-
-  uint32_t my = kNone;  // local selection index of this lane's team
-  uint32_t q = 0;       // round within the selection
-  unsigned long long pool_next = 0, pool_end = 0;
-  bool exhausted = false;
-
-  while (true) {
-    uint32_t need = __ballot_sync(kFull, leader && my == kNone);
-    while (need != 0u && !exhausted) {
-      if (pool_next >= pool_end) {
-        unsigned long long base = 0;
-        if (lane == 0u) base = atomicAdd(&P.ctr->next, grab);
-        base = __shfl_sync(kFull, base, 0);
-        if (base >= K) {
-          exhausted = true;
-          break;
-        }
-        pool_next = base;
-        pool_end = min(base + grab, (unsigned long long)K);
-      }
-      const uint32_t avail = (uint32_t)(pool_end - pool_next);
-      const uint32_t r = __popc(need & lanemask_lt());
-      uint32_t mine = kNone;
-      if (((need >> lane) & 1u) && r < avail) mine = (uint32_t)pool_next + r;
-      const uint32_t got = __shfl_sync(kFull, mine, tbase);
-      if (got != kNone) {
-        my = got;
-        q = 0;
-      }
-      pool_next += min((uint32_t)__popc(need), avail);
-      need = __ballot_sync(kFull, leader && my == kNone);
-    }
-    if (exhausted && __all_sync(kFull, my == kNone)) break;
-
-    const bool active = my != kNone;
-    const uint32_t c = q * g + rank;
-    const Philox4 x = philox4x32_10(c, P.s0 + my, P.epoch, kTagTrials, P.seed_lo, P.seed_hi);
-    const uint32_t j0 = __umulhi(x.x, M);
-    const uint32_t j1 = __umulhi(x.z, M);
-    const float t0 = __fmul_rn(unit24(x.y), amax);
-    const float t1 = __fmul_rn(unit24(x.w), amax);
-    const bool a0 = active && c < calls && accept<PATH>(t0, j0, smem, P.alpha, P.group_shift);
-    const bool a1 = active && !a0 && c < half && accept<PATH>(t1, j1, smem, P.alpha, P.group_shift);
-    const uint32_t b = __ballot_sync(kFull, a0 || a1) & tmask;
-    const uint32_t src = b ? (uint32_t)(__ffs(b) - 1) : lane;
-    const uint32_t pick_j = a0 ? j0 : j1;
-    const uint32_t pick_t = a0 ? 2u * c + 1u : 2u * c + 2u;
-    const uint32_t wj = __shfl_sync(kFull, pick_j, src);
-    const uint32_t wt = __shfl_sync(kFull, pick_t, src);
-    const bool out_of_calls = (q + 1u) * g >= calls;
-    if (active) {
-      if (b != 0u || out_of_calls) {
-        if (leader) {
-          P.idx[my] = b ? (int32_t)wj : -1;
-          if (P.trials) P.trials[my] = b ? wt : P.max_trials;
-        }
-        my = kNone;
-      } else {
-        ++q;
-      }
-    }
+  const uint32_t K = P.K;
+  const uint32_t nwarps = nthreads >> 5;
+  const uint32_t warp_global = tid >> 5;
+  const uint32_t g = choose_team(st.p, K, nwarps);
+  // grab: ~8192 expected trials per atomic (st.grab), but never more than a quarter of a
+  // warp's fair share so every warp gets work; at least one selection per team.
+  const unsigned long long teams = 32u / g;
+  const unsigned long long fair = (unsigned long long)K / nwarps;
+  unsigned long long grab = min((unsigned long long)st.grab, max(teams, fair / 4ull));
+  grab = max(grab, 1ull);
+  Pool pl;
+  pl.grab = grab;
+  pl.next = (unsigned long long)warp_global * grab;  // static first chunk, no atomic
+  pl.end = min(pl.next + grab, (unsigned long long)K);
+  pl.base_next = (unsigned long long)nwarps * grab;
+  pl.exhausted = pl.next >= K;
+  const TrialStream ts(P.seed_lo, P.seed_hi, P.epoch);
+  const bool fold = can_fold(st.amax_bits);
+  if (g == 1u) {
+    if (fold)
+      trial_loop<PATH, true, false>(P, ts, sbase, amax, 1u, pl);
+    else
+      trial_loop<PATH, false, false>(P, ts, sbase, amax, 1u, pl);
+  } else {
+    if (fold)
+      trial_loop<PATH, true, true>(P, ts, sbase, amax, g, pl);
+    else
+      trial_loop<PATH, false, true>(P, ts, sbase, amax, g, pl);
   }
 
   // ---- the last CTA out resets the work-stealing ticket for the next launch

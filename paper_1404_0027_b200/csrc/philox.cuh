@@ -21,30 +21,79 @@ struct Philox4 {
   uint32_t x, y, z, w;
 };
 
-// Ten rounds of (hi0,lo0) = M0*c0, (hi1,lo1) = M1*c2, c = (hi1^c1^k0, lo1, hi0^c3^k1, lo0),
-// key += Weyl between rounds.  Fully unrolled; mul.wide.u32 gives hi and lo in one
-// IMAD.WIDE.U32.
+// One round: (hi0,lo0) = M0*c0, (hi1,lo1) = M1*c2, c = (hi1^c1^k0, lo1, hi0^c3^k1, lo0).
+// mul.wide.u32 gives hi and lo in one IMAD.WIDE.U32.
+__device__ __forceinline__ void philox_round(uint32_t& c0, uint32_t& c1, uint32_t& c2, uint32_t& c3, uint32_t k0,
+                                             uint32_t k1) {
+  const uint64_t p0 = (uint64_t)kPhiloxM0 * c0;
+  const uint64_t p1 = (uint64_t)kPhiloxM1 * c2;
+  const uint32_t hi0 = (uint32_t)(p0 >> 32), lo0 = (uint32_t)p0;
+  const uint32_t hi1 = (uint32_t)(p1 >> 32), lo1 = (uint32_t)p1;
+  c0 = hi1 ^ c1 ^ k0;
+  c1 = lo1;
+  c2 = hi0 ^ c3 ^ k1;
+  c3 = lo0;
+}
+
+// Ten rounds; key += Weyl constants between rounds.
 __device__ __forceinline__ Philox4 philox4x32_10(uint32_t c0, uint32_t c1, uint32_t c2, uint32_t c3,
                                                  uint32_t k0, uint32_t k1) {
 #pragma unroll
   for (int r = 0; r < 10; ++r) {
-    const uint64_t p0 = (uint64_t)kPhiloxM0 * c0;
-    const uint64_t p1 = (uint64_t)kPhiloxM1 * c2;
-    const uint32_t hi0 = (uint32_t)(p0 >> 32), lo0 = (uint32_t)p0;
-    const uint32_t hi1 = (uint32_t)(p1 >> 32), lo1 = (uint32_t)p1;
-    c0 = hi1 ^ c1 ^ k0;
-    c1 = lo1;
-    c2 = hi0 ^ c3 ^ k1;
-    c3 = lo0;
+    philox_round(c0, c1, c2, c3, k0, k1);
     k0 += kPhiloxW0;
     k1 += kPhiloxW1;
   }
   return Philox4{c0, c1, c2, c3};
 }
 
+// The trial stream with everything that is invariant hoisted: counter = {c, s, epoch, 0}.
+// Round 1 of M1*c2 involves only the epoch (warp-uniform), and c1 = s, c3 = 0, so round 1
+// collapses to one IMAD.WIDE: c0' = hi(M1*epoch) ^ s ^ k0, c1' = lo(M1*epoch),
+// c2' = hi(M0*c) ^ k1, c3' = lo(M0*c).  Rounds 2..10 use precomputed round keys.  The
+// output is bit-identical to philox4x32_10(c, s, epoch, 0, k0, k1) (same arithmetic).
+struct TrialStream {
+  uint32_t rk0[10], rk1[10];  // round keys (warp-uniform)
+  uint32_t e_hi_k0;           // hi(M1*epoch) ^ k0
+  uint32_t e_lo;              // lo(M1*epoch)
+
+  __device__ __forceinline__ TrialStream(uint32_t seed_lo, uint32_t seed_hi, uint32_t epoch) {
+#pragma unroll
+    for (int r = 0; r < 10; ++r) {
+      rk0[r] = seed_lo + (uint32_t)r * kPhiloxW0;
+      rk1[r] = seed_hi + (uint32_t)r * kPhiloxW1;
+    }
+    const uint64_t p1 = (uint64_t)kPhiloxM1 * epoch;
+    e_hi_k0 = (uint32_t)(p1 >> 32) ^ seed_lo;
+    e_lo = (uint32_t)p1;
+  }
+
+  // per-selection constant of round 1
+  __device__ __forceinline__ uint32_t sel_word(uint32_t s) const { return e_hi_k0 ^ s; }
+
+  __device__ __forceinline__ Philox4 operator()(uint32_t c, uint32_t sel) const {
+    const uint64_t p0 = (uint64_t)kPhiloxM0 * c;
+    uint32_t c0 = sel, c1 = e_lo, c2 = (uint32_t)(p0 >> 32) ^ rk1[0], c3 = (uint32_t)p0;
+#pragma unroll
+    for (int r = 1; r < 10; ++r) philox_round(c0, c1, c2, c3, rk0[r], rk1[r]);
+    return Philox4{c0, c1, c2, c3};
+  }
+};
+
 // u = (x >> 8) * 2^-24 in [0,1): 24 random bits, exact in binary32 (R3).
 __device__ __forceinline__ float unit24(uint32_t x) {
   return __fmul_rn(__uint2float_rn(x >> 8), 0x1p-24f);
+}
+
+// fl32(u * amax) for u = (x >> 8) 2^-24.  With amax_s = amax * 2^-24 exact (amax >=
+// 2^-102, so no underflow), (x>>8) * amax_s is the same real product, hence the same
+// round-to-nearest result, with one multiply instead of two.
+template <bool FOLD>
+__device__ __forceinline__ float scaled_u(uint32_t x, float amax, float amax_s) {
+  if constexpr (FOLD)
+    return __fmul_rn(__uint2float_rn(x >> 8), amax_s);
+  else
+    return __fmul_rn(unit24(x), amax);
 }
 
 // u1 = (2 (x >> 9) + 1) * 2^-24 in (0,1) (R10).
@@ -57,5 +106,8 @@ __device__ __forceinline__ float neg_log_u1(uint32_t seed_lo, uint32_t seed_hi, 
   const Philox4 t = philox4x32_10(0u, s, epoch, kTagTau, seed_lo, seed_hi);
   return -logf(unit24_open(t.x));
 }
+
+// amax >= 2^-102  <=>  amax * 2^-24 is a normal binary32 (exact scaling)
+__device__ __forceinline__ bool can_fold(uint32_t amax_bits) { return amax_bits >= 0x0C800000u; }
 
 }  // namespace gpuar
