@@ -111,6 +111,21 @@ int gpuar_select(gpuar_t h, int64_t K, int32_t *d_idx, float *d_tau, uint32_t *d
 int gpuar_select_host(gpuar_t h, const float *h_alpha, int64_t rows, int64_t ld, int64_t K,
                       int32_t *h_idx, float *h_tau, uint32_t *h_trials);
 
+/* Selection rule (R1, R16-R19).
+ *   GPUAR_RULE_CLASSIC (default, w must be 1): classic AR with first accept, the hot path
+ *     described at the top of this header; samples alpha_j / alpha_0.
+ *   GPUAR_RULE_ARGMIN (w >= 1): the paper's printed GPU algorithm (PAPER.md:304-380,
+ *     pseudo-code PAPER.md:498-560): T = fl32(w * alpha_max); every reaction j draws v_j
+ *     (Philox counter {j >> 2, s_g, epoch, 3}, word j & 3, v = (x >> 8) 2^-24),
+ *     u_j = fl32(v_j T), eligible iff u_j < alpha_j with rating R_j = fl32(u_j / alpha_j),
+ *     else R_j = 1; idx = argmin_j R_j (ties to the lowest j), -1 if min R >= 1; trials = M.
+ *     Its law is NOT alpha_j / alpha_0 (R1).
+ * Applies to later gpuar_select / gpuar_select_host calls (shared vector and matrix).
+ * Errors: EINVAL (unknown rule, w out of range). */
+#define GPUAR_RULE_CLASSIC 0
+#define GPUAR_RULE_ARGMIN  1
+int gpuar_set_rule(gpuar_t h, int rule, float w);
+
 /* Global index of local selection 0 (sharding: rank r of G -> r*K/G).  s0 in [0, 2^32). */
 int gpuar_set_selection_offset(gpuar_t h, int64_t s0);
 

@@ -80,6 +80,10 @@ def _load():
             ctypes.c_uint64, ctypes.c_uint32, ctypes.c_uint32, ctypes.c_void_p, ctypes.c_void_p,
             ctypes.c_void_p, ctypes.c_int]
         lib.oracle_argmin_batch.restype = ctypes.c_int
+        lib.oracle_election.argtypes = [ctypes.c_float, ctypes.c_float, ctypes.c_float]
+        lib.oracle_election.restype = ctypes.c_float
+        lib.oracle_selection.argtypes = [ctypes.c_void_p, ctypes.c_int64]
+        lib.oracle_selection.restype = ctypes.c_int32
         lib.oracle_histogram.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int64,
                                          ctypes.c_int64, ctypes.c_void_p, ctypes.c_void_p]
         lib.oracle_histogram.restype = None
@@ -186,6 +190,17 @@ def it_select(alpha, K: int, seed: int, epoch: int = 0, s0: int = 0,
     idx = np.empty(K, np.int32)
     _load().oracle_it_batch(_ptr(a), M, rows, ld, K, seed & (2**64 - 1), s0, epoch, _ptr(idx), nthreads)
     return idx
+
+
+def election(alpha_j: float, v: float, T: float) -> float:
+    """Election step: R = fl32(v T)/alpha_j if fl32(v T) < alpha_j else 1."""
+    return float(_load().oracle_election(alpha_j, v, T))
+
+
+def selection(ratings) -> int:
+    """Selection step: argmin, ties to the lowest index, -1 if min >= 1."""
+    r = _f32(ratings)
+    return int(_load().oracle_selection(_ptr(r), r.size))
 
 
 def argmin_select(alpha, K: int, seed: int, w: float = 1.0, epoch: int = 0, s0: int = 0,

@@ -296,6 +296,28 @@ int oracle_it_batch(const float *alpha, int64_t M, int64_t rows, int64_t ld, int
  *   selection: j* = argmin_j R_j, ties to the lowest j;
  *     if R_j* >= 1 the election failed: rejected (idx -1; the paper's M+1).
  * trials = M (draws consumed). tau as for the classic rule. */
+/* Election step: rating of reaction j for unit draw v_j. */
+float oracle_election(float alpha_j, float v, float T)
+{
+    float u = v * T;                               /* u_{0,T} in [0, T) */
+    return (u < alpha_j) ? u / alpha_j : 1.0f;     /* R >= 1 means "not eligible" */
+}
+
+/* Selection step: argmin of the ratings, ties to the lowest
+ * index; -1 when the minimum is >= 1 (the election failed: rejection). */
+int32_t oracle_selection(const float *R, int64_t M)
+{
+    float best = 1.0f;
+    int32_t best_j = -1;
+    for (int64_t j = 0; j < M; ++j) {
+        if (R[j] < best) {
+            best = R[j];
+            best_j = (int32_t)j;
+        }
+    }
+    return best_j;
+}
+
 void oracle_argmin_one(const float *alpha, int64_t M, float amax, double a0, float w,
                        uint64_t seed, uint32_t s, uint32_t epoch,
                        int32_t *idx, float *tau, double *tau_ref)
@@ -312,11 +334,8 @@ void oracle_argmin_one(const float *alpha, int64_t M, float amax, double a0, flo
     uint32_t x[4];
     for (int64_t j = 0; j < M; ++j) {
         if ((j & 3) == 0) draw(seed, (uint32_t)(j >> 2), s, epoch, 3u, x);
-        float v = oracle_unit(x[j & 3]);
-        float u = v * T;
-        float R = 1.0f;
-        if (u < alpha[j]) R = u / alpha[j];
-        if (R < best) {           /* strict: ties keep the lowest index */
+        float R = oracle_election(alpha[j], oracle_unit(x[j & 3]), T);
+        if (R < best) {           /* oracle_selection, streamed: strict, ties keep the lowest j */
             best = R;
             best_j = (int32_t)j;
         }

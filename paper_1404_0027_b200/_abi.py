@@ -12,6 +12,7 @@ import os
 from . import _build
 
 OK, EINVAL, ENOMEM, ECUDA, ENOTSET, EPROPENSITY = 0, -1, -2, -3, -4, -5
+RULE_CLASSIC, RULE_ARGMIN = 0, 1
 
 _vp = ctypes.c_void_p
 _i64 = ctypes.c_int64
@@ -28,6 +29,7 @@ SIGNATURES = {
     "gpuar_set_propensities": (_int, [_vp, _vp, _i64, _i64]),
     "gpuar_select": (_int, [_vp, _i64, _vp, _vp, _vp]),
     "gpuar_select_host": (_int, [_vp, _vp, _i64, _i64, _i64, _vp, _vp, _vp]),
+    "gpuar_set_rule": (_int, [_vp, _int, ctypes.c_float]),
     "gpuar_set_selection_offset": (_int, [_vp, _i64]),
     "gpuar_set_epoch": (_int, [_vp, _u32]),
     "gpuar_get_epoch": (_int, [_vp, ctypes.POINTER(_u32)]),

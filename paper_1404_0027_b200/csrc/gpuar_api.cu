@@ -70,6 +70,11 @@ struct gpuar_handle {
   uint32_t stage_bytes = 0;
   // shared policy
   int sh_block = 256, sh_grid = 0;
+  // selection rule (gpuar_set_rule)
+  int rule = kRuleClassic;
+  float w = 1.0f;
+  int am_grid = 0;
+  bool am_smem = true;
   Chunked host;
 };
 
@@ -174,7 +179,11 @@ int launch_select(gpuar_handle* h, const float* alpha, int64_t rows, int64_t ld,
     p.n_pref = h->n_pref;
     p.group_shift = h->group_shift;
     p.smem_bytes = h->shared_smem;
-    e = launch_select_shared(p, h->shared_path, h->sh_grid, h->sh_block, st);
+    p.w = h->w;
+    if (h->rule == kRuleArgmin)
+      e = launch_argmin_shared(p, h->am_smem, h->am_grid, 256, st);
+    else
+      e = launch_select_shared(p, h->shared_path, h->sh_grid, h->sh_block, st);
   } else {
     RowsParams p{};
     p.alpha = alpha;
@@ -193,6 +202,8 @@ int launch_select(gpuar_handle* h, const float* alpha, int64_t rows, int64_t ld,
     p.stages = (uint32_t)h->rows_stages;
     p.stage_bytes = h->stage_bytes;
     p.stats_only = 0;
+    p.rule = h->rule;
+    p.w = h->w;
     const int grid = (int)std::min<int64_t>(h->rows_grid, (K + h->rows_warps - 1) / h->rows_warps);
     e = launch_select_rows(p, std::max(grid, 1), h->rows_warps, st);
   }
@@ -256,6 +267,12 @@ int gpuar_create(gpuar_t* out, int64_t M, int64_t K, uint64_t seed) {
   cudaDeviceGetAttribute(&h->smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, h->device);
   set_select_shared_limits(h->smem_optin);
   set_select_rows_limits(h->smem_optin);
+  set_argmin_limits(h->smem_optin);
+  {
+    const size_t am_sh = (size_t)((M + 3) & ~3ll) * 4u;
+    h->am_smem = am_sh + 1024u <= (size_t)h->smem_optin;
+    h->am_grid = h->num_sms * 8;  // 8 x 256 threads per SM (occupancy-capped by the runtime)
+  }
   // stats launch shape depends on M only -> identical reduction tree on every rank
   h->stats_blocks = (int)std::min<int64_t>((M + 4095) / 4096, 512);
   plan_shared(h);
@@ -440,6 +457,20 @@ int gpuar_select_host(gpuar_t h, const float* h_alpha, int64_t rows, int64_t ld,
   }
   ++h->epoch;
   return check_err_flag(h);
+}
+
+int gpuar_set_rule(gpuar_t h, int rule, float w) {
+  if (!h) return GPUAR_EINVAL;
+  if (rule == GPUAR_RULE_CLASSIC) {
+    if (w != 1.0f) return GPUAR_EINVAL;
+  } else if (rule == GPUAR_RULE_ARGMIN) {
+    if (!(w >= 1.0f) || !std::isfinite(w)) return GPUAR_EINVAL;
+  } else {
+    return GPUAR_EINVAL;
+  }
+  h->rule = rule;
+  h->w = w;
+  return GPUAR_OK;
 }
 
 int gpuar_set_selection_offset(gpuar_t h, int64_t s0) {

@@ -36,6 +36,11 @@ enum Path : int {
   kPathRows = 4,       // per-realization K x M matrix, bulk-async staged rows
 };
 
+enum Rule : int {
+  kRuleClassic = 0,  // classic AR, first accept (the north_star hot path)
+  kRuleArgmin = 1,   // the paper's printed election + argmin selection
+};
+
 struct SharedParams {
   const float* alpha;        // M floats (device)
   const uint16_t* prefilter; // paths 2/3: bf16 codes (device)
@@ -53,6 +58,7 @@ struct SharedParams {
   uint32_t n_pref;           // number of prefilter entries (paths 2/3)
   uint32_t group_shift;      // path 3: log2(group size)
   uint32_t smem_bytes;       // bytes of the staged vector / prefilter
+  float w;                   // argmin rule: T = fl32(w * alpha_max)
 };
 
 struct RowsParams {
@@ -73,6 +79,8 @@ struct RowsParams {
   uint32_t stages;           // ring depth per warp
   uint32_t stage_bytes;      // bytes per ring slot (multiple of 16)
   uint32_t stats_only;       // 1: gpuar_row_stats (no trials)
+  int rule;                  // kRuleClassic / kRuleArgmin
+  float w;                   // argmin rule: T = fl32(w * alpha_max)
 };
 
 // ---------------------------------------------------------------- PTX helpers
@@ -131,6 +139,12 @@ __device__ __forceinline__ float lds_f32(uint32_t addr) {
   return v;
 }
 
+__device__ __forceinline__ float4 lds_f32x4(uint32_t addr) {
+  float4 v;
+  asm("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(addr));
+  return v;
+}
+
 __device__ __forceinline__ uint32_t lds_u16(uint32_t addr) {
   unsigned short v;
   asm("ld.shared.u16 %0, [%1];" : "=h"(v) : "r"(addr));
@@ -150,6 +164,8 @@ cudaError_t launch_stats(const float* alpha, uint32_t M, double* part_sum, uint3
 cudaError_t launch_prefilter(const float* alpha, uint32_t M, uint16_t* pref, uint32_t n_pref,
                              uint32_t group_shift, int path, cudaStream_t st);
 cudaError_t launch_select_shared(const SharedParams& p, int path, int grid, int block, cudaStream_t st);
+cudaError_t launch_argmin_shared(const SharedParams& p, bool smem, int grid, int block, cudaStream_t st);
+void set_argmin_limits(int bytes);
 cudaError_t launch_select_rows(const RowsParams& p, int grid, int warps, cudaStream_t st);
 cudaError_t launch_histogram(const int32_t* idx, const uint32_t* trials, uint32_t K, uint32_t M,
                              unsigned long long* hist, unsigned long long* totals, int grid,

@@ -53,6 +53,32 @@ __device__ __forceinline__ void row_trials(const TrialStream& ts, uint32_t sel, 
   }
 }
 
+// The paper's printed rule on one row (R16-R19): lane l rates reactions 4c..4c+3
+// of its calls c = l, l+32, ...; warp butterfly on the (rating bits, index) key.
+template <bool FOLD>
+__device__ __forceinline__ void row_argmin(const TrialStream& ts, uint32_t sel, uint32_t row_s, uint32_t M, float T,
+                                           uint32_t lane, int32_t& id) {
+  const float T_s = __fmul_rn(T, 0x1p-24f);
+  const uint32_t k1t = ts.rk1[0] ^ kTagElection;
+  const uint32_t calls = (M + 3u) >> 2;
+  unsigned long long best = ((unsigned long long)0x3f800000u << 32) | 0xffffffffull;
+  for (uint32_t c = lane; c < calls; c += 32u) {
+    const Philox4 x = ts.with_tag(c, sel, k1t);
+    const uint32_t xs[4] = {x.x, x.y, x.z, x.w};
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const uint32_t j = 4u * c + q;
+      const float d = j < M ? lds_f32(row_s + 4u * j) : 0.f;
+      const float t = scaled_u<FOLD>(xs[q], T, T_s);
+      const float R = (t < d) ? __fdiv_rn(t, d) : 1.0f;
+      best = min(best, ((unsigned long long)__float_as_uint(R) << 32) | j);
+    }
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) best = min(best, __shfl_xor_sync(kFull, best, o));
+  id = (uint32_t)(best >> 32) < 0x3f800000u ? (int32_t)(uint32_t)best : -1;
+}
+
 template <int MAXW>
 __global__ void __launch_bounds__(MAXW * 32, 1) select_rows_kernel(const RowsParams P) {
   extern __shared__ __align__(128) unsigned char smem[];
@@ -155,11 +181,19 @@ __global__ void __launch_bounds__(MAXW * 32, 1) select_rows_kernel(const RowsPar
         const float amax = __uint_as_float(mx);
         tau = __fdiv_rn(nl, __double2float_rn(acc));
         const uint32_t sel = ts.sel_word(P.s0 + (uint32_t)r);
-        if (can_fold(mx))
+        if (P.rule == kRuleArgmin) {
+          // the paper's printed rule on this row: election + argmin selection
+          const float T = __fmul_rn(P.w, amax);
+          if (can_fold(__float_as_uint(T)))
+            row_argmin<true>(ts, sel, row_s, M, T, lane, id);
+          else
+            row_argmin<false>(ts, sel, row_s, M, T, lane, id);
+          tr = M;
+        } else if (can_fold(mx))
           row_trials<true>(ts, sel, row_s, M, amax, half, calls, lane, id, tr);
         else
           row_trials<false>(ts, sel, row_s, M, amax, half, calls, lane, id, tr);
-        if (id < 0) tr = P.max_trials;
+        if (id < 0 && P.rule == kRuleClassic) tr = P.max_trials;
       }
       if (lane == 0) {
         P.idx[r] = id;

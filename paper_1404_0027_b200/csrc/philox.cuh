@@ -16,6 +16,7 @@ constexpr uint32_t kPhiloxW1 = 0xBB67AE85u;
 // Stream tags (counter word 3), R12.
 constexpr uint32_t kTagTrials = 0u;
 constexpr uint32_t kTagTau = 1u;
+constexpr uint32_t kTagElection = 3u;  // the paper's argmin rule: call j >> 2, word j & 3
 
 struct Philox4 {
   uint32_t x, y, z, w;
@@ -47,17 +48,19 @@ __device__ __forceinline__ Philox4 philox4x32_10(uint32_t c0, uint32_t c1, uint3
   return Philox4{c0, c1, c2, c3};
 }
 
-// The trial stream with everything that is invariant hoisted: counter = {c, s, epoch, 0}.
-// Round 1 of M1*c2 involves only the epoch (warp-uniform), and c1 = s, c3 = 0, so round 1
+// The trial stream with everything that is invariant hoisted: counter = {c, s, epoch, tag}.
+// Round 1 of M1*c2 involves only the epoch (warp-uniform), and c1 = s, c3 = tag, so round 1
 // collapses to one IMAD.WIDE: c0' = hi(M1*epoch) ^ s ^ k0, c1' = lo(M1*epoch),
-// c2' = hi(M0*c) ^ k1, c3' = lo(M0*c).  Rounds 2..10 use precomputed round keys.  The
-// output is bit-identical to philox4x32_10(c, s, epoch, 0, k0, k1) (same arithmetic).
+// c2' = hi(M0*c) ^ tag ^ k1, c3' = lo(M0*c).  Rounds 2..10 use precomputed round keys.  The
+// output is bit-identical to philox4x32_10(c, s, epoch, tag, k0, k1) (same arithmetic).
 struct TrialStream {
   uint32_t rk0[10], rk1[10];  // round keys (warp-uniform)
   uint32_t e_hi_k0;           // hi(M1*epoch) ^ k0
   uint32_t e_lo;              // lo(M1*epoch)
+  uint32_t k1_tag;            // k1 ^ tag (counter word 3 enters round 1 only)
 
-  __device__ __forceinline__ TrialStream(uint32_t seed_lo, uint32_t seed_hi, uint32_t epoch) {
+  __device__ __forceinline__ TrialStream(uint32_t seed_lo, uint32_t seed_hi, uint32_t epoch,
+                                         uint32_t tag = kTagTrials) {
 #pragma unroll
     for (int r = 0; r < 10; ++r) {
       rk0[r] = seed_lo + (uint32_t)r * kPhiloxW0;
@@ -66,14 +69,18 @@ struct TrialStream {
     const uint64_t p1 = (uint64_t)kPhiloxM1 * epoch;
     e_hi_k0 = (uint32_t)(p1 >> 32) ^ seed_lo;
     e_lo = (uint32_t)p1;
+    k1_tag = seed_hi ^ tag;
   }
 
   // per-selection constant of round 1
   __device__ __forceinline__ uint32_t sel_word(uint32_t s) const { return e_hi_k0 ^ s; }
 
-  __device__ __forceinline__ Philox4 operator()(uint32_t c, uint32_t sel) const {
+  __device__ __forceinline__ Philox4 operator()(uint32_t c, uint32_t sel) const { return with_tag(c, sel, k1_tag); }
+
+  // same stream family with another tag: k1t = seed_hi ^ tag
+  __device__ __forceinline__ Philox4 with_tag(uint32_t c, uint32_t sel, uint32_t k1t) const {
     const uint64_t p0 = (uint64_t)kPhiloxM0 * c;
-    uint32_t c0 = sel, c1 = e_lo, c2 = (uint32_t)(p0 >> 32) ^ rk1[0], c3 = (uint32_t)p0;
+    uint32_t c0 = sel, c1 = e_lo, c2 = (uint32_t)(p0 >> 32) ^ k1t, c3 = (uint32_t)p0;
 #pragma unroll
     for (int r = 1; r < 10; ++r) philox_round(c0, c1, c2, c3, rk0[r], rk1[r]);
     return Philox4{c0, c1, c2, c3};

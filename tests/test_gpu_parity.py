@@ -327,3 +327,70 @@ def test_bench_philox_runs():
     sel.bench_philox(1024, 8, sink)
     sel.sync()
     assert sink.abs().sum().item() > 0
+
+
+# ---------------------------------------------------------------- the paper's printed rule (NEXT-1)
+
+def _argmin_case(alpha, K, w=1.0, epoch=0, s0=0):
+    a = np.asarray(alpha, np.float32)
+    sel = _sel(a.shape[-1], K)
+    sel.set_rule("argmin", w)
+    sel.set_selection_offset(s0)
+    sel.epoch = epoch
+    sel.set_propensities(torch.from_numpy(a).cuda())
+    out = sel.select(K)
+    sel.sync()
+    ref = oracle.argmin_select(a, K, seed=SEED, w=w, epoch=epoch, s0=s0, nthreads=8)
+    return out, ref
+
+
+@pytest.mark.parametrize("M", [4, 5, 64, 256, 1024, 1029])
+@pytest.mark.parametrize("w", [1.0, 2.0])
+def test_argmin_shared_gaussian(M, w):
+    a = synth.discrete_gaussian(M) if M > 5 else np.arange(1, M + 1, dtype=np.float32)
+    out, ref = _argmin_case(a, 20_000, w=w, epoch=3, s0=777)
+    np.testing.assert_array_equal(out[0].cpu().numpy(), ref["idx"])
+    assert (out[2].cpu().numpy() == M).all()
+    rel = np.abs(out[1].cpu().numpy() - ref["tau_ref"]) / ref["tau_ref"]
+    assert rel.max() <= TAU_RTOL
+    if w == 1.0:
+        assert (out[0].cpu() >= 0).all()          # zero rejection at w = 1
+
+
+def test_argmin_shared_law_gpu():
+    a = np.asarray([1, 2, 3, 4], np.float32)
+    out, _ = _argmin_case(a, 200_000)
+    h = np.bincount(out[0].cpu().numpy(), minlength=4)
+    assert oracle.chi2_pvalue(h, oracle.argmin_law(a))[1] > 0.001
+
+
+def test_argmin_large_vector_global_path():
+    a = synth.exponential(70_000)
+    out, ref = _argmin_case(a, 300, w=1.5)
+    np.testing.assert_array_equal(out[0].cpu().numpy(), ref["idx"])
+
+
+def test_argmin_rows():
+    M, K = 1029, 3000
+    host = synth.rows(synth.yeast_rates(M), synth.GEN_SEED, 0, K)
+    host[5, :] = 0.0
+    for w in (1.0, 1.5):
+        sel = _sel(M, K)
+        sel.set_rule("argmin", w)
+        sel.set_propensities(torch.from_numpy(host).cuda())
+        idx, tau, trials = sel.select(K)
+        sel.sync()
+        ref = oracle.argmin_select(host, K, seed=SEED, w=w, nthreads=8)
+        np.testing.assert_array_equal(idx.cpu().numpy(), ref["idx"])
+        fin = np.isfinite(ref["tau_ref"])
+        rel = np.abs(tau.cpu().numpy()[fin] - ref["tau_ref"][fin]) / ref["tau_ref"][fin]
+        assert rel.max() <= TAU_RTOL
+
+
+def test_set_rule_validation():
+    from paper_1404_0027_b200 import GpuarError
+    sel = _sel(4, 4)
+    with pytest.raises(GpuarError):
+        sel.set_rule("classic", 2.0)
+    with pytest.raises(GpuarError):
+        sel.set_rule("argmin", 0.5)
