@@ -48,6 +48,10 @@ CONFIGS = {
                desc="c4: per-realization KxM matrix, M=1029 yeast-like rows, K=2^20 realizations per GPU"),
     "c5": dict(kind="shared", dist="pareto", M=1_000_000, K=1 << 21,
                desc="c5: M=1e6 Pareto(1.5) shared vector, K=2^21 selections per GPU (2^24 at 8 GPUs)"),
+    # NEXT-2: the full SSA loop (propensities + selection + state update) on chip
+    "s1": dict(kind="ssa", dist="yeast-network", M=1029, K=1 << 17, inner=16,
+               desc="s1: full SSA steps, yeast-like mass-action network (641 species, 1029 reactions), "
+                    "K=2^17 realizations per GPU, 16 steps per launch"),
     # NEXT-1: the paper's printed election + argmin rule on its own Table 1 / Fig. 2 workload
     "p1": dict(kind="shared", dist="gaussian", M=1024, K=62_500, rule="argmin",
                desc="p1: paper's argmin rule, discrete Gaussian M=1024, K=62500 parallel realizations"),
@@ -185,6 +189,12 @@ def make_inputs(w: dict, rank: int, device):
 
     import synth
     M, K = w["M"], w["K"]
+    if w["kind"] == "ssa":
+        net = synth.yeast_like_network(M=M)
+        dev = {k: torch.from_numpy(np.ascontiguousarray(net[k])).to(device) for k in ("reac", "rate", "didx", "dval")}
+        X = torch.from_numpy(synth.initial_state(net["N"], K)).to(device)
+        t = torch.zeros(K, dtype=torch.float64, device=device)
+        return dict(net=dev, N=net["N"], X=X, t=t)
     if w["kind"] == "rows":
         import synth.gpu as sg
         rates = torch.from_numpy(synth.yeast_rates(M)).to(device)
@@ -202,6 +212,9 @@ def host_sample(w: dict, rank: int, n: int):
     import numpy as np
 
     import synth
+    if w["kind"] == "ssa":
+        net = synth.yeast_like_network(M=w["M"])
+        return net, synth.initial_state(net["N"], n)
     if w["kind"] == "rows":
         return synth.rows(synth.yeast_rates(w["M"]), synth.GEN_SEED, rank * w["K"], n)
     if w["dist"] == "hand":
@@ -211,25 +224,36 @@ def host_sample(w: dict, rank: int, n: int):
 
 def oracle_rate(w: dict, seconds: float, threads: int, max_rows: int | None = None):
     """Oracle selections/s on a bounded sample of the workload (rank 0's first selections)."""
+    import numpy as np
+
     import oracle
+
+    def run(n):
+        if w["kind"] == "ssa":
+            net, X0 = host_sample(w, 0, n)
+            t0 = time.perf_counter()
+            r = oracle.ssa_run(net, X0, np.zeros(n), w["inner"], seed=20140327, nthreads=threads)
+            return time.perf_counter() - t0, int(r["steps"].sum())
+        alpha = host_sample(w, 0, n)
+        t0 = time.perf_counter()
+        if w.get("rule") == "argmin":
+            oracle.argmin_select(alpha, n, seed=20140327, w=w["w"], nthreads=threads)
+        else:
+            oracle.ar_select(alpha, n, seed=20140327, nthreads=threads)
+        return time.perf_counter() - t0, n
+
     probe = 256
     K = w["K"]
     while True:
         n = min(probe, K)
-        alpha = host_sample(w, 0, n)
-        t0 = time.perf_counter()
-        oracle.ar_select(alpha, n, seed=20140327, nthreads=threads)
-        dt = time.perf_counter() - t0
+        dt, _ = run(n)
         if dt > 0.25 or n == K:
             break
         probe *= 4
     target = int(n * seconds / max(dt, 1e-9))
     n = max(1, min(K, target, max_rows or K))
-    alpha = host_sample(w, 0, n)
-    t0 = time.perf_counter()
-    oracle.ar_select(alpha, n, seed=20140327, nthreads=threads)
-    dt = time.perf_counter() - t0
-    return n / dt, n, dt
+    dt, units = run(n)
+    return units / dt, n, dt
 
 
 # ----------------------------------------------------------------- the reference (oracle) arm
@@ -412,6 +436,71 @@ def run_gpuar(args, w, rank, world, local_rank):
     sel.close()
 
 
+def run_ssa(args, w, rank, world, local_rank):
+    """NEXT-2 workload: K realizations advance `inner` SSA steps per launch (gpuar_ssa_run)."""
+    import torch
+
+    from paper_1404_0027_b200 import Selector
+    from paper_1404_0027_b200.dist import max_over_ranks, weak_shard
+
+    device = torch.device("cuda", local_rank)
+    torch.cuda.set_device(device)
+    M, K, inner = w["M"], w["K"], w["inner"]
+    inp = make_inputs(w, rank, device)
+    sel = Selector(M, K, 20140327, device=local_rank)
+    sel.set_selection_offset(weak_shard(K, rank)[0])
+    n = inp["net"]
+    sel.set_network(n["reac"], n["rate"], n["didx"], n["dval"], inp["N"])
+    X, t = inp["X"], inp["t"]
+    steps = torch.zeros(K, dtype=torch.int32, device=device)
+    for _ in range(max(args.warmup, 3)):
+        sel.ssa_run(X, t, inner, steps=steps)
+    sel.sync()
+    total = torch.zeros(K, dtype=torch.int64, device=device)
+    stream = torch.cuda.current_stream(device)
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local_rank) as clk:
+        clk.wait_first()
+        if world > 1:
+            torch.distributed.barrier()
+        torch.cuda.synchronize()
+        t_start = time.perf_counter()
+        ev0.record(stream)
+        for _ in range(args.steps):
+            sel.ssa_run(X, t, inner, steps=steps)
+            total += steps
+        ev1.record(stream)
+        ev1.synchronize()
+        t_end = time.perf_counter()
+        time.sleep(0.06)
+        clk.mark(t_start, t_end)
+    sel.sync()
+    ms = max_over_ranks(ev0.elapsed_time(ev1), device)
+    events = int(total.sum().item())
+    events_all = int(max_over_ranks(float(events), device)) * world  # weak scaling: equal work per rank
+    value = events_all / (ms * 1e-3)
+    if rank == 0:
+        cpu = None
+        if world == 1 and not args.no_cpu:
+            threads = os.cpu_count() or 1
+            rate, nn, dt = oracle_rate(w, args.cpu_seconds, threads)
+            cpu = {"value": rate, "unit": "SSA events/s", "cores": threads, "kind": "oracle",
+                   "sample": f"{nn} realizations x {inner} steps from the initial state ({dt:.1f} s)"}
+        res = {"metric": METRIC, "value": value, "unit": "SSA events/s (one selection each)", "n_gpus": world,
+               "steps": args.steps, "warmup": max(args.warmup, 3), "ms_per_step": ms / args.steps,
+               "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+               "data": "synthetic (seeded synth/ network and initial state)",
+               "config": {"workload": w["desc"], "M": M, "N": inp["N"], "K_per_gpu": K, "steps_per_launch": inner},
+               "roofline": {"bound": "alu", "achieved": value / 1e9, "peak": None, "unit": "G SSA events/s",
+                            "frac": None, "traffic": None,
+                            "note": "on-chip: per event M mass-action propensities + reductions + AR trials; "
+                                    "no HBM traffic but the state in/out per launch"},
+               "cpu_baseline": cpu, "e2e": None, "gpu_launches": args.steps, "clocks": clk.summary(),
+               "validation": {"events": events, "events_per_realization_per_launch": events / K / args.steps}}
+        print(json.dumps(res), flush=True)
+    sel.close()
+
+
 def main():
     args = parse()
     w = workload(args)
@@ -431,7 +520,10 @@ def main():
         else:
             dist.init_process_group(args.dist_backend)
     try:
-        run_gpuar(args, w, rank, world, local_rank)
+        if w["kind"] == "ssa":
+            run_ssa(args, w, rank, world, local_rank)
+        else:
+            run_gpuar(args, w, rank, world, local_rank)
     finally:
         if world > 1:
             dist.destroy_process_group()

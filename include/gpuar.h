@@ -126,6 +126,26 @@ int gpuar_select_host(gpuar_t h, const float *h_alpha, int64_t rows, int64_t ld,
 #define GPUAR_RULE_ARGMIN  1
 int gpuar_set_rule(gpuar_t h, int rule, float w);
 
+/* NEXT-2: the full SSA loop around the selector.
+ * gpuar_set_network registers a mass-action network of N species and the handle's M
+ * reactions (device pointers, BORROWED): d_reac[M][2] reactant species (-1 = none; equal
+ * entries = dimerisation), d_rate[M] rate constants, d_didx[M][D] / d_dval[M][D] the sparse
+ * change vector v_j (species -1 = unused slot; species distinct within a reaction).
+ * Propensity a_j = c_j, c_j X_a, c_j X_a X_b, or c_j X_a (X_a - 1) / 2 (+0 if X_a < 2), in
+ * binary32 left to right (R20).  The network plus one realization's state and
+ * row (4M + 4N bytes) must fit in shared memory (EINVAL otherwise).
+ * gpuar_ssa_run advances K realizations (d_X[K][N] int32 and d_t[K] binary64, in place)
+ * by up to n_steps steps each: step i of realization k (selection s_g = offset + k) uses
+ * epoch + i: propensities, classic-AR selection and tau exactly as gpuar_select on that
+ * row; alpha_0 = 0 -> halted; t + tau > t_end -> halted (state kept); a rejected
+ * selection fires nothing (R21); else X += v_j, t += tau.  d_steps[k] (may be
+ * NULL) receives the number of events fired.  Then epoch += n_steps.  Asynchronous.
+ * Errors: EINVAL, ENOTSET (no network), ECUDA; invalid propensities -> sticky EPROPENSITY. */
+int gpuar_set_network(gpuar_t h, int64_t N, int64_t D, const int32_t *d_reac, const float *d_rate,
+                      const int32_t *d_didx, const int32_t *d_dval);
+int gpuar_ssa_run(gpuar_t h, int32_t *d_X, double *d_t, uint32_t *d_steps, int64_t K, int32_t n_steps,
+                  double t_end);
+
 /* Global index of local selection 0 (sharding: rank r of G -> r*K/G).  s0 in [0, 2^32). */
 int gpuar_set_selection_offset(gpuar_t h, int64_t s0);
 

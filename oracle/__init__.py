@@ -84,6 +84,13 @@ def _load():
         lib.oracle_election.restype = ctypes.c_float
         lib.oracle_selection.argtypes = [ctypes.c_void_p, ctypes.c_int64]
         lib.oracle_selection.restype = ctypes.c_int32
+        lib.oracle_propensity.argtypes = [ctypes.c_void_p, ctypes.c_int32, ctypes.c_int32, ctypes.c_float]
+        lib.oracle_propensity.restype = ctypes.c_float
+        lib.oracle_ssa_run.argtypes = [
+            ctypes.c_int64, ctypes.c_int64, ctypes.c_int64, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p,
+            ctypes.c_void_p, ctypes.c_int64, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int32,
+            ctypes.c_double, ctypes.c_uint64, ctypes.c_uint32, ctypes.c_uint32, ctypes.c_uint32, ctypes.c_int]
+        lib.oracle_ssa_run.restype = ctypes.c_int
         lib.oracle_histogram.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int64,
                                          ctypes.c_int64, ctypes.c_void_p, ctypes.c_void_p]
         lib.oracle_histogram.restype = None
@@ -247,6 +254,31 @@ def argmin_law(alpha, w: float = 1.0, reject: bool = False):
     if reject:
         return P, float(np.prod(1.0 - d))
     return P
+
+
+def propensity(X, r0: int, r1: int, c: float) -> float:
+    """Mass-action propensity (R20)."""
+    x = np.ascontiguousarray(X, np.int32)
+    return float(_load().oracle_propensity(_ptr(x), r0, r1, c))
+
+
+def ssa_run(net: dict, X0, t0, n_steps: int, seed: int, t_end: float = float("inf"), epoch0: int = 0,
+            s0: int = 0, max_trials: int = 1 << 20, nthreads: int = 1) -> dict:
+    """K SSA realizations of the network net = {reac (M,2) int32,
+    rate (M,) float32, didx (M,D) int32, dval (M,D) int32}; X0 (K,N) int32, t0 (K,) float64.
+    Returns X, t, steps (events fired) and the status."""
+    reac = np.ascontiguousarray(net["reac"], np.int32)
+    rate = _f32(net["rate"])
+    didx = np.ascontiguousarray(net["didx"], np.int32)
+    dval = np.ascontiguousarray(net["dval"], np.int32)
+    X = np.array(X0, dtype=np.int32, order="C", copy=True)
+    t = np.array(t0, dtype=np.float64, copy=True)
+    K, N = X.shape
+    M, D = didx.shape
+    steps = np.zeros(K, np.uint32)
+    st = _load().oracle_ssa_run(N, M, D, _ptr(reac), _ptr(rate), _ptr(didx), _ptr(dval), K, _ptr(X), _ptr(t),
+                                _ptr(steps), n_steps, t_end, seed & (2**64 - 1), s0, epoch0, max_trials, nthreads)
+    return dict(X=X, t=t, steps=steps, status=int(st))
 
 
 def histogram(idx, trials, M: int) -> tuple[np.ndarray, int]:

@@ -30,6 +30,9 @@
  *      u1 = (2*(x>>9)+1) * 2^-24 in (0,1) from its own Philox stream (tag 1).
  *   4. Inverse-transform linear search, the classic direct method the paper
  *      replaces: smallest j with sum_{j'<=j} alpha_j' > u2*alpha_0.
+ *   5. (NEXT-1) the paper's printed election + argmin rule.
+ *   6. (NEXT-2) the full SSA loop around the selector: mass-action
+ *      propensities, selection, X += v_j, t += tau.
  *
  * Philox4x32-10 is the counter-based generator of Salmon et al. (SC'11, "Parallel
  * random numbers: as easy as 1, 2, 3"), written out from its definition; the
@@ -46,6 +49,7 @@
 #include <math.h>
 #include <stdint.h>
 #include <stddef.h>
+#include <stdlib.h>
 
 #if !defined(FLT_EVAL_METHOD) || FLT_EVAL_METHOD != 0
 #error "oracle needs FLT_EVAL_METHOD == 0 (binary32 evaluated in binary32)"
@@ -375,6 +379,86 @@ int oracle_argmin_batch(const float *alpha, int64_t M, int64_t rows, int64_t ld,
             continue;
         }
         oracle_argmin_one(row, M, amax, a0, w, seed, s0 + (uint32_t)r, epoch, &idx[r], &tau[r], &tau_ref[r]);
+    }
+    return status;
+}
+
+/* ------------------------------------------------------------------ full SSA (NEXT-2) */
+
+/* Mass-action propensity of a reaction with reactants r0, r1 (species index, -1 = none)
+ * and rate constant c (Gillespie's direct method; "propensity function
+ * a_j", updated at each step):  order 0: c;  order 1: c X_r0;  two different species:
+ * c X_r0 X_r1;  dimerisation (r0 == r1): c X (X-1) / 2, and +0 when X < 2.  binary32,
+ * evaluated left to right (R20). */
+float oracle_propensity(const int32_t *X, int32_t r0, int32_t r1, float c)
+{
+    float a = c;
+    if (r0 >= 0) {
+        if (r1 == r0) {
+            int32_t x = X[r0];
+            if (x < 2) return 0.0f;
+            a = a * (float)x;
+            a = a * (float)(x - 1);
+            return a * 0.5f;
+        }
+        a = a * (float)X[r0];
+    }
+    if (r1 >= 0) a = a * (float)X[r1];
+    return a;
+}
+
+/* K independent SSA realizations (propensities, next reaction and tau,
+ * "the system is updated using v_j, t <- t + tau", until t_end).  Realization k (global
+ * selection index s0 + k) makes up to n_steps steps; step i uses epoch epoch0 + i:
+ *   a_j = propensity(X_k) for every j; (idx, tau) = classic AR selection on that row;
+ *   a0 = 0            -> halted (nothing can fire), state kept;
+ *   t + tau > t_end   -> halted (the next event is past t_end), state kept;
+ *   idx = -1 (rejected after max_trials) -> no event this step (R21);
+ *   else X += v_idx (D sparse (species, delta) pairs, species -1 = unused), t += tau.
+ * X is K x N int32 (in/out), t is K doubles (in/out), steps[k] = events fired.
+ * Returns ORACLE_EPROPENSITY if a propensity was invalid (negative/non-finite). */
+int oracle_ssa_run(int64_t N, int64_t M, int64_t D, const int32_t *reac, const float *rate,
+                   const int32_t *didx, const int32_t *dval, int64_t K, int32_t *X, double *t,
+                   uint32_t *steps, int32_t n_steps, double t_end, uint64_t seed, uint32_t s0,
+                   uint32_t epoch0, uint32_t max_trials, int nthreads)
+{
+    int status = ORACLE_OK;
+#pragma omp parallel num_threads(nthreads > 0 ? nthreads : 1)
+    {
+        float *row = (float *)malloc(sizeof(float) * (size_t)M);
+#pragma omp for schedule(dynamic, 16)
+        for (int64_t k = 0; k < K; ++k) {
+            int32_t *x = X + k * N;
+            uint32_t fired = 0;
+            for (int32_t i = 0; i < n_steps; ++i) {
+                for (int64_t j = 0; j < M; ++j)
+                    row[j] = oracle_propensity(x, reac[2 * j], reac[2 * j + 1], rate[j]);
+                float amax;
+                double a0;
+                if (oracle_stats(row, M, &amax, &a0) != ORACLE_OK) {
+#pragma omp atomic write
+                    status = ORACLE_EPROPENSITY;
+                    break;
+                }
+                if (amax == 0.0f) break;                      /* halted: nothing can fire */
+                int32_t idx;
+                uint32_t tr;
+                float tau;
+                double tau_ref;
+                oracle_ar_one(row, M, amax, a0, seed, s0 + (uint32_t)k, epoch0 + (uint32_t)i, max_trials,
+                              &idx, &tr, &tau, &tau_ref);
+                if (t[k] + (double)tau > t_end) break;       /* next event past t_end */
+                if (idx < 0) continue;                        /* rejected: no event this step */
+                for (int64_t d = 0; d < D; ++d) {
+                    int32_t sp = didx[idx * D + d];
+                    if (sp >= 0) x[sp] += dval[idx * D + d];
+                }
+                t[k] += (double)tau;
+                ++fired;
+            }
+            steps[k] = fired;
+        }
+        free(row);
     }
     return status;
 }

@@ -30,6 +30,8 @@ SIGNATURES = {
     "gpuar_select": (_int, [_vp, _i64, _vp, _vp, _vp]),
     "gpuar_select_host": (_int, [_vp, _vp, _i64, _i64, _i64, _vp, _vp, _vp]),
     "gpuar_set_rule": (_int, [_vp, _int, ctypes.c_float]),
+    "gpuar_set_network": (_int, [_vp, _i64, _i64, _vp, _vp, _vp, _vp]),
+    "gpuar_ssa_run": (_int, [_vp, _vp, _vp, _vp, _i64, _i32, ctypes.c_double]),
     "gpuar_set_selection_offset": (_int, [_vp, _i64]),
     "gpuar_set_epoch": (_int, [_vp, _u32]),
     "gpuar_get_epoch": (_int, [_vp, ctypes.POINTER(_u32)]),

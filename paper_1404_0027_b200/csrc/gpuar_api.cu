@@ -66,7 +66,7 @@ struct gpuar_handle {
   int num_sms = 148;
   int smem_optin = 227 * 1024;
   // rows policy
-  int rows_warps = 0, rows_stages = 0, rows_grid = 0;
+  int rows_warps = 0, rows_stages = 0, rows_grid = 0, rows_lb = 2;
   uint32_t stage_bytes = 0;
   // shared policy
   int sh_block = 256, sh_grid = 0;
@@ -75,6 +75,14 @@ struct gpuar_handle {
   float w = 1.0f;
   int am_grid = 0;
   bool am_smem = true;
+  // SSA network (gpuar_set_network), borrowed device pointers
+  const int32_t* net_reac = nullptr;
+  const float* net_rate = nullptr;
+  const int32_t* net_didx = nullptr;
+  const int32_t* net_dval = nullptr;
+  int64_t net_N = 0, net_D = 0;
+  int ssa_warps = 0, ssa_grid = 0;
+  uint32_t ssa_net_bytes = 0, ssa_warp_bytes = 0;
   Chunked host;
 };
 
@@ -149,6 +157,7 @@ int plan_rows(gpuar_handle* h) {
   if (!fits(W, S) || S > 32) return GPUAR_EINVAL;  // M too large for the row pipeline
   h->rows_warps = W;
   h->rows_stages = S;
+  h->rows_lb = std::max(0, std::min(5, env_int("GPUAR_ROWS_LOG2_BLOCK", 2)));
   h->stage_bytes = (uint32_t)sb;
   const size_t sh = (((size_t)W * S * 8u + 127u) & ~(size_t)127u) + (size_t)W * S * sb;
   const int n = select_rows_blocks_per_sm(W, sh);
@@ -204,7 +213,9 @@ int launch_select(gpuar_handle* h, const float* alpha, int64_t rows, int64_t ld,
     p.stats_only = 0;
     p.rule = h->rule;
     p.w = h->w;
-    const int grid = (int)std::min<int64_t>(h->rows_grid, (K + h->rows_warps - 1) / h->rows_warps);
+    p.log2_block = (uint32_t)h->rows_lb;
+    const int64_t per_cta = (int64_t)h->rows_warps << h->rows_lb;
+    const int grid = (int)std::min<int64_t>(h->rows_grid, (K + per_cta - 1) / per_cta);
     e = launch_select_rows(p, std::max(grid, 1), h->rows_warps, st);
   }
   return cuda_status(e);
@@ -268,6 +279,7 @@ int gpuar_create(gpuar_t* out, int64_t M, int64_t K, uint64_t seed) {
   set_select_shared_limits(h->smem_optin);
   set_select_rows_limits(h->smem_optin);
   set_argmin_limits(h->smem_optin);
+  set_ssa_limits(h->smem_optin);
   {
     const size_t am_sh = (size_t)((M + 3) & ~3ll) * 4u;
     h->am_smem = am_sh + 1024u <= (size_t)h->smem_optin;
@@ -473,6 +485,68 @@ int gpuar_set_rule(gpuar_t h, int rule, float w) {
   return GPUAR_OK;
 }
 
+int gpuar_set_network(gpuar_t h, int64_t N, int64_t D, const int32_t* d_reac, const float* d_rate,
+                      const int32_t* d_didx, const int32_t* d_dval) {
+  if (!h || !d_reac || !d_rate || !d_didx || !d_dval || N < 1 || N > 0x7fffffffll || D < 1 || D > 32)
+    return GPUAR_EINVAL;
+  const uint64_t M = (uint64_t)h->M;
+  const uint64_t net = ((M * (8u + 4u + 8u * (uint64_t)D)) + 15u) & ~15ull;
+  const uint64_t per_warp = ((4u * M + 15u) & ~15ull) + ((4u * (uint64_t)N + 15u) & ~15ull);
+  const uint64_t budget = (uint64_t)h->smem_optin - 1024u;
+  if (net + per_warp > budget) return GPUAR_EINVAL;  // network + one realization must fit on chip
+  int W = (int)std::min<uint64_t>(24, (budget - net) / per_warp);
+  const size_t sh = (size_t)net + (size_t)W * per_warp;
+  DeviceGuard g(h->device);
+  if (!g.ok) return GPUAR_ECUDA;
+  const int n = ssa_blocks_per_sm(W, sh);
+  if (n <= 0) return GPUAR_EINVAL;
+  h->net_reac = d_reac;
+  h->net_rate = d_rate;
+  h->net_didx = d_didx;
+  h->net_dval = d_dval;
+  h->net_N = N;
+  h->net_D = D;
+  h->ssa_warps = W;
+  h->ssa_grid = n * h->num_sms;
+  h->ssa_net_bytes = (uint32_t)net;
+  h->ssa_warp_bytes = (uint32_t)per_warp;
+  return GPUAR_OK;
+}
+
+int gpuar_ssa_run(gpuar_t h, int32_t* d_X, double* d_t, uint32_t* d_steps, int64_t K, int32_t n_steps, double t_end) {
+  if (!h || !d_X || !d_t || K < 1 || K > h->Kcap || n_steps < 0) return GPUAR_EINVAL;
+  if (!h->net_reac) return GPUAR_ENOTSET;
+  if (h->offset + (uint64_t)K > (1ull << 32)) return GPUAR_EINVAL;
+  DeviceGuard g(h->device);
+  if (!g.ok) return GPUAR_ECUDA;
+  SsaParams p{};
+  p.reac = h->net_reac;
+  p.rate = h->net_rate;
+  p.didx = h->net_didx;
+  p.dval = h->net_dval;
+  p.X = d_X;
+  p.t = d_t;
+  p.steps = d_steps;
+  p.ctr = h->d_ctr;
+  p.t_end = t_end;
+  p.N = (uint32_t)h->net_N;
+  p.M = (uint32_t)h->M;
+  p.D = (uint32_t)h->net_D;
+  p.K = (uint32_t)K;
+  p.s0 = (uint32_t)h->offset;
+  p.epoch0 = h->epoch;
+  p.seed_lo = (uint32_t)h->seed;
+  p.seed_hi = (uint32_t)(h->seed >> 32);
+  p.max_trials = h->max_trials;
+  p.n_steps = n_steps;
+  p.net_bytes = h->ssa_net_bytes;
+  p.warp_bytes = h->ssa_warp_bytes;
+  const int grid = (int)std::min<int64_t>(h->ssa_grid, (K + h->ssa_warps - 1) / h->ssa_warps);
+  const int st = cuda_status(launch_ssa(p, std::max(grid, 1), h->ssa_warps, h->stream));
+  if (st == GPUAR_OK) h->epoch += (uint32_t)n_steps;
+  return st;
+}
+
 int gpuar_set_selection_offset(gpuar_t h, int64_t s0) {
   if (!h || s0 < 0 || s0 > 0xffffffffll) return GPUAR_EINVAL;
   h->offset = (uint64_t)s0;
@@ -534,7 +608,9 @@ int gpuar_row_stats(gpuar_t h, float* d_amax, double* d_a0) {
   p.stages = (uint32_t)h->rows_stages;
   p.stage_bytes = h->stage_bytes;
   p.stats_only = 1;
-  const int grid = (int)std::min<int64_t>(h->rows_grid, (h->rows + h->rows_warps - 1) / h->rows_warps);
+  p.log2_block = (uint32_t)h->rows_lb;
+  const int64_t per_cta = (int64_t)h->rows_warps << h->rows_lb;
+  const int grid = (int)std::min<int64_t>(h->rows_grid, (h->rows + per_cta - 1) / per_cta);
   return cuda_status(launch_select_rows(p, std::max(grid, 1), h->rows_warps, h->stream));
 }
 

@@ -22,10 +22,11 @@ struct DevStats {
 };
 
 // Per-handle device counters.
+constexpr uint32_t kStripes = 16;  // work-stealing tickets, one per stripe of selections
 struct DevCounters {
-  unsigned long long next;  // work-stealing ticket (reset by the last CTA of each launch)
-  unsigned int done;        // CTAs finished in the current launch
-  unsigned int err;         // sticky EPROPENSITY flag (cleared by the host)
+  unsigned long long next[kStripes];  // tickets (reset by the last CTA of each launch)
+  unsigned int done;                  // CTAs finished in the current launch
+  unsigned int err;                   // sticky EPROPENSITY flag (cleared by the host)
 };
 
 enum Path : int {
@@ -81,9 +82,30 @@ struct RowsParams {
   uint32_t stats_only;       // 1: gpuar_row_stats (no trials)
   int rule;                  // kRuleClassic / kRuleArgmin
   float w;                   // argmin rule: T = fl32(w * alpha_max)
+  uint32_t log2_block;       // rows per warp block = 2^log2_block (<= 32)
+};
+
+struct SsaParams {
+  const int32_t* reac;   // M x 2 reactant species (-1 = none)
+  const float* rate;     // M mass-action constants
+  const int32_t* didx;   // M x D state-change species (-1 = unused)
+  const int32_t* dval;   // M x D state-change values
+  int32_t* X;            // K x N copy numbers (in/out)
+  double* t;             // K times (in/out)
+  uint32_t* steps;       // K events fired (out, may be null)
+  DevCounters* ctr;
+  double t_end;
+  uint32_t N, M, D, K;
+  uint32_t s0, epoch0, seed_lo, seed_hi, max_trials;
+  int32_t n_steps;
+  uint32_t net_bytes;    // staged network (smem)
+  uint32_t warp_bytes;   // per-warp row + state (smem)
 };
 
 // ---------------------------------------------------------------- PTX helpers
+// Shared-memory loads by 32-bit shared-window address (no generic->shared conversion per
+// access).  volatile + "memory": never hoisted above the barriers / bulk-copy waits /
+// stores that produce the data (ring slots and SSA rows are rewritten in place).
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
@@ -135,19 +157,26 @@ __device__ __forceinline__ void fence_proxy_async_smem() {
 
 __device__ __forceinline__ float lds_f32(uint32_t addr) {
   float v;
-  asm("ld.shared.f32 %0, [%1];" : "=f"(v) : "r"(addr));
+  asm volatile("ld.shared.f32 %0, [%1];" : "=f"(v) : "r"(addr) : "memory");
   return v;
 }
 
 __device__ __forceinline__ float4 lds_f32x4(uint32_t addr) {
   float4 v;
-  asm("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(addr));
+  asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(addr)
+               : "memory");
+  return v;
+}
+
+__device__ __forceinline__ uint32_t lds_u32(uint32_t addr) {
+  uint32_t v;
+  asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(addr) : "memory");
   return v;
 }
 
 __device__ __forceinline__ uint32_t lds_u16(uint32_t addr) {
   unsigned short v;
-  asm("ld.shared.u16 %0, [%1];" : "=h"(v) : "r"(addr));
+  asm volatile("ld.shared.u16 %0, [%1];" : "=h"(v) : "r"(addr) : "memory");
   return v;
 }
 
@@ -166,6 +195,9 @@ cudaError_t launch_prefilter(const float* alpha, uint32_t M, uint16_t* pref, uin
 cudaError_t launch_select_shared(const SharedParams& p, int path, int grid, int block, cudaStream_t st);
 cudaError_t launch_argmin_shared(const SharedParams& p, bool smem, int grid, int block, cudaStream_t st);
 void set_argmin_limits(int bytes);
+cudaError_t launch_ssa(const SsaParams& p, int grid, int warps, cudaStream_t st);
+int ssa_blocks_per_sm(int warps, size_t smem);
+void set_ssa_limits(int bytes);
 cudaError_t launch_select_rows(const RowsParams& p, int grid, int warps, cudaStream_t st);
 cudaError_t launch_histogram(const int32_t* idx, const uint32_t* trials, uint32_t K, uint32_t M,
                              unsigned long long* hist, unsigned long long* totals, int grid,

@@ -90,7 +90,7 @@ __global__ void __launch_bounds__(kStatsThreads) stats_pass2(const double* part_
     s.grab = grab;
     s.pad = 0;
     *stats = s;
-    ctr->next = 0ull;
+    for (uint32_t i = 0; i < kStripes; ++i) ctr->next[i] = 0ull;
     ctr->done = 0u;
     if (!s.valid) atomicOr(&ctr->err, 1u);
   }

@@ -99,8 +99,15 @@ __global__ void __launch_bounds__(MAXW * 32, 1) select_rows_kernel(const RowsPar
   const uint64_t K = P.K;
   const uint32_t M = P.M;
   const uint64_t row_bytes = P.ld * 4ull;
-  // row handled by this warp at its n-th step: CTAs take consecutive blocks of W rows
-  auto row_of = [&](uint32_t n) -> uint64_t { return ((uint64_t)n * G + blockIdx.x) * warps + warp; };
+  // Row handled by this warp at its n-th step: warps take turns on blocks of B = 2^lb
+  // consecutive rows (block (n/B)*WT + wg), so the rows in flight over the whole GPU stay
+  // within a window of B*WT rows (B = 4: ~58 MB, inside the 256 MB TLB reach) while a warp's
+  // outputs for a block go out as one store per output array from B lanes.
+  const uint64_t WT = G * warps;
+  const uint64_t wg = (uint64_t)blockIdx.x * warps + warp;
+  const uint32_t lb = P.log2_block;
+  const uint32_t bm = (1u << lb) - 1u;
+  auto row_of = [&](uint32_t n) -> uint64_t { return ((((uint64_t)(n >> lb)) * WT + wg) << lb) + (n & bm); };
   auto issue = [&](uint32_t n, uint32_t slot) {
     const uint64_t off = row_of(n) * row_bytes;
     const uint64_t a = off & ~15ull;
@@ -118,8 +125,12 @@ __global__ void __launch_bounds__(MAXW * 32, 1) select_rows_kernel(const RowsPar
   const uint32_t half = P.max_trials >> 1;
   const uint32_t calls = half + (P.max_trials & 1u);
   const TrialStream ts(P.seed_lo, P.seed_hi, P.epoch);
-  const uint32_t full_chunks = M >> 8;  // 256 elements = 8 per lane
   float nlog = 0.f;                     // -ln(u1) of row_of(n0 + lane)
+  // this lane's buffered outputs for row (block base + lane)
+  int32_t o_id = -1;
+  uint32_t o_tr = 0;
+  float o_tau = 0.f;
+  double o_a0 = 0.0;
 
   for (uint32_t n = 0;; ++n) {
     const uint64_t r = row_of(n);
@@ -131,12 +142,17 @@ __global__ void __launch_bounds__(MAXW * 32, 1) select_rows_kernel(const RowsPar
       nlog = rr < K ? neg_log_u1(P.seed_lo, P.seed_hi, P.s0 + (uint32_t)rr, P.epoch) : 0.f;
     }
     mbar_wait(&bars[slot], parity);
-    const float* row = reinterpret_cast<const float*>(ring + (size_t)slot * SB + ((r * row_bytes) & 15ull));
+    // The slot holds the row's 16-byte hull: element j sits at word lead + j.
+    const uint32_t lead = (uint32_t)((r * row_bytes) & 15ull) >> 2;
+    const uint32_t row_s = smem_u32(ring + (size_t)slot * SB) + 4u * lead;
 
-    // ---- alpha_max (max of bit patterns) and alpha_0
-    const uint32_t row_s = smem_u32(row);
+    // ---- alpha_max (max of bit patterns) and alpha_0: 8 scalar LDS per lane per chunk of
+    // 256 (conflict-free, consecutive lanes), pairwise binary32 sum of the 8 promoted to
+    // binary64.  (A 16-byte-vector variant with hull edge handling measured 3 % more
+    // instructions and 5 % slower: profiles/r01_c4_select_rows_v3.md.)
     uint32_t mx = 0;
     double acc = 0.0;
+    const uint32_t full_chunks = M >> 8;
     for (uint32_t ch = 0; ch < full_chunks; ++ch) {
       const uint32_t p = row_s + 4u * (ch * 256u + lane);
       float v[8];
@@ -162,10 +178,11 @@ __global__ void __launch_bounds__(MAXW * 32, 1) select_rows_kernel(const RowsPar
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(kFull, acc, o);
 
+    const uint32_t nl32 = n & bm;  // this row's slot in the block's output buffer
     if (P.stats_only) {
-      if (lane == 0) {
-        P.amax_out[r] = mx < kInfBits ? __uint_as_float(mx) : __uint_as_float(0x7fc00000u);
-        P.a0_out[r] = mx < kInfBits ? acc : __longlong_as_double(0x7ff8000000000000ll);
+      if (lane == nl32) {
+        o_tau = mx < kInfBits ? __uint_as_float(mx) : __uint_as_float(0x7fc00000u);
+        o_a0 = mx < kInfBits ? acc : __longlong_as_double(0x7ff8000000000000ll);
       }
     } else {
       const float nl = __shfl_sync(kFull, nlog, n & 31u);
@@ -195,10 +212,23 @@ __global__ void __launch_bounds__(MAXW * 32, 1) select_rows_kernel(const RowsPar
           row_trials<false>(ts, sel, row_s, M, amax, half, calls, lane, id, tr);
         if (id < 0 && P.rule == kRuleClassic) tr = P.max_trials;
       }
-      if (lane == 0) {
-        P.idx[r] = id;
-        if (P.tau) P.tau[r] = tau;
-        if (P.trials) P.trials[r] = tr;
+      if (lane == nl32) {
+        o_id = id;
+        o_tau = tau;
+        o_tr = tr;
+      }
+    }
+    if (nl32 == bm || r + 1u >= K) {  // flush the block: one coalesced store per output
+      const uint64_t rl = r - nl32 + lane;
+      if (lane <= nl32) {
+        if (P.stats_only) {
+          P.amax_out[rl] = o_tau;
+          P.a0_out[rl] = o_a0;
+        } else {
+          P.idx[rl] = o_id;
+          if (P.tau) P.tau[rl] = o_tau;
+          if (P.trials) P.trials[rl] = o_tr;
+        }
       }
     }
     __syncwarp();

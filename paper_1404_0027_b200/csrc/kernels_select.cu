@@ -46,28 +46,62 @@ __device__ __forceinline__ bool accept(float t, uint32_t j, uint32_t sbase, cons
   }
 }
 
+// Work distribution: the K selections are cut into kStripes contiguous stripes; warp w
+// belongs to stripe w % kStripes, takes a static first chunk of it, then grabs `grab`
+// selections at a time from the stripe's ticket until the stripe is exhausted.  kStripes
+// tickets keep same-address atomic contention low; a warp never leaves its stripe (a
+// stripe holds K/16 selections, so stripes finish within ~1/sqrt(K/16) of each other),
+// so each warp makes at most one failing atomic.
 struct Pool {
-  unsigned long long next, end, grab, base_next;
+  unsigned long long next, end;  // current chunk [next, end)
+  unsigned long long grab, first;
+  uint32_t K, nwarps, stripe;
   bool exhausted;
+
+  __device__ __forceinline__ unsigned long long stripe_lo(uint32_t s) const {
+    const unsigned long long sz = ((unsigned long long)K + kStripes - 1) / kStripes;
+    return min((unsigned long long)s * sz, (unsigned long long)K);
+  }
+  __device__ __forceinline__ unsigned long long stripe_hi(uint32_t s) const { return stripe_lo(s + 1); }
+  // start of the dynamic part of stripe s (after its warps' static chunks)
+  __device__ __forceinline__ unsigned long long dyn_base(uint32_t s) const {
+    const unsigned long long nw = (nwarps > s) ? (nwarps - s + kStripes - 1) / kStripes : 0;
+    return stripe_lo(s) + nw * first;
+  }
 };
 
-// Hand idle teams (leader lanes in `need`) the next selections of the warp's pool,
-// refilling it with one atomic per `grab` selections.  Returns the new selection of this
-// lane's team (broadcast from its leader) or kNone.
-__device__ __forceinline__ uint32_t pool_take(Pool& pl, uint32_t need, uint32_t lane, uint32_t tbase, uint32_t K,
+__device__ __forceinline__ void pool_init(Pool& pl, uint32_t K, uint32_t nwarps, uint32_t warp_global,
+                                          unsigned long long first, unsigned long long grab) {
+  pl.K = K;
+  pl.nwarps = nwarps;
+  pl.first = first;
+  pl.grab = grab;
+  pl.stripe = warp_global % kStripes;
+  const unsigned long long hi = pl.stripe_hi(pl.stripe);
+  const unsigned long long lo = pl.stripe_lo(pl.stripe) + (unsigned long long)(warp_global / kStripes) * first;
+  pl.next = min(lo, hi);
+  pl.end = min(lo + first, hi);
+  // nothing static and no dynamic part left in the stripe: done without touching the ticket
+  pl.exhausted = pl.next >= pl.end && pl.dyn_base(pl.stripe) >= hi;
+}
+
+// Hand idle teams (leader lanes in `need`) the next selections of the warp's pool.
+// Returns the new selection of this lane's team (broadcast from its leader) or kNone.
+__device__ __forceinline__ uint32_t pool_take(Pool& pl, uint32_t need, uint32_t lane, uint32_t tbase,
                                               DevCounters* ctr) {
   uint32_t got = kNone;
   while (need != 0u && !pl.exhausted) {
     if (pl.next >= pl.end) {
       unsigned long long b = 0;
-      if (lane == 0u) b = pl.base_next + atomicAdd(&ctr->next, pl.grab);
+      if (lane == 0u) b = pl.dyn_base(pl.stripe) + atomicAdd(&ctr->next[pl.stripe], pl.grab);
       b = __shfl_sync(kFull, b, 0);
-      if (b >= K) {
+      const unsigned long long hi = pl.stripe_hi(pl.stripe);
+      if (b >= hi) {  // stripe exhausted
         pl.exhausted = true;
         break;
       }
       pl.next = b;
-      pl.end = min(b + pl.grab, (unsigned long long)K);
+      pl.end = min(b + pl.grab, hi);
     }
     const uint32_t avail = (uint32_t)(pl.end - pl.next);
     const uint32_t r = __popc(need & lanemask_lt());
@@ -75,8 +109,7 @@ __device__ __forceinline__ uint32_t pool_take(Pool& pl, uint32_t need, uint32_t 
     if (((need >> lane) & 1u) && r < avail) mine = (uint32_t)pl.next + r;
     mine = __shfl_sync(kFull, mine, tbase);
     if (mine != kNone) got = mine;
-    const uint32_t taken = min((uint32_t)__popc(need), avail);
-    pl.next += taken;
+    pl.next += min((uint32_t)__popc(need), avail);
     // leaders that got work drop out of `need`
     const uint32_t served = __ballot_sync(kFull, ((need >> lane) & 1u) && r < avail);
     need &= ~served;
@@ -91,7 +124,7 @@ template <int PATH, bool FOLD, bool TEAM>
 __device__ __forceinline__ void trial_loop(const SharedParams& P, const TrialStream& ts, uint32_t sbase, float amax,
                                            uint32_t g, Pool pl) {
   const float amax_s = __fmul_rn(amax, 0x1p-24f);
-  const uint32_t M = P.M, K = P.K;
+  const uint32_t M = P.M;
   const uint32_t half = P.max_trials >> 1;            // calls whose odd trial is < max_trials
   const uint32_t calls = half + (P.max_trials & 1u);  // calls whose even trial is < max_trials
   const uint32_t lane = threadIdx.x & 31u;
@@ -107,7 +140,7 @@ __device__ __forceinline__ void trial_loop(const SharedParams& P, const TrialStr
   while (true) {
     const uint32_t need = __ballot_sync(kFull, leader && my == kNone);
     if (need != 0u) {
-      const uint32_t got = pool_take(pl, need, lane, tbase, K, P.ctr);
+      const uint32_t got = pool_take(pl, need, lane, tbase, P.ctr);
       if (got != kNone) {
         my = got;
         sel = ts.sel_word(P.s0 + got);
@@ -230,18 +263,14 @@ __global__ void __launch_bounds__(1024, 1) select_shared_kernel(const SharedPara
   const uint32_t nwarps = nthreads >> 5;
   const uint32_t warp_global = tid >> 5;
   const uint32_t g = choose_team(st.p, K, nwarps);
-  // grab: ~8192 expected trials per atomic (st.grab), but never more than a quarter of a
-  // warp's fair share so every warp gets work; at least one selection per team.
+  // static first chunk: half of a warp's fair share; then grabs of ~8192 expected trials
+  // (st.grab), at most an eighth of the fair share, at least one selection per team.
   const unsigned long long teams = 32u / g;
-  const unsigned long long fair = (unsigned long long)K / nwarps;
-  unsigned long long grab = min((unsigned long long)st.grab, max(teams, fair / 4ull));
-  grab = max(grab, 1ull);
+  const unsigned long long fair = max(1ull, (unsigned long long)K / nwarps);
+  const unsigned long long first = max(teams, fair / 2ull);
+  const unsigned long long grab = max(2ull * teams, min((unsigned long long)st.grab, fair / 8ull));
   Pool pl;
-  pl.grab = grab;
-  pl.next = (unsigned long long)warp_global * grab;  // static first chunk, no atomic
-  pl.end = min(pl.next + grab, (unsigned long long)K);
-  pl.base_next = (unsigned long long)nwarps * grab;
-  pl.exhausted = pl.next >= K;
+  pool_init(pl, K, nwarps, warp_global, first, grab);
   const TrialStream ts(P.seed_lo, P.seed_hi, P.epoch);
   const bool fold = can_fold(st.amax_bits);
   if (g == 1u) {
@@ -262,7 +291,7 @@ __global__ void __launch_bounds__(1024, 1) select_shared_kernel(const SharedPara
     __threadfence();
     const unsigned int prev = atomicAdd(&P.ctr->done, 1u);
     if (prev == gridDim.x - 1u) {
-      P.ctr->next = 0ull;
+      for (uint32_t i = 0; i < kStripes; ++i) P.ctr->next[i] = 0ull;
       P.ctr->done = 0u;
       __threadfence();
     }

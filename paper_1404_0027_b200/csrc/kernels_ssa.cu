@@ -1,0 +1,179 @@
+// kernels_ssa.cu -- NEXT-2: the full SSA loop around the selector:
+// "two uniform random numbers u1 and u2 ... tau = (1/a0) ln(1/u1) ... the index j of the
+// next reaction ... Then the system is updated using v_j, t <- t + tau", with the next
+// reaction chosen by the classic AR hot path.
+//
+// One warp owns one realization at a time; its state X (N int32) and its propensity row
+// (M binary32) live in the warp's shared-memory slice, the reaction network (reactants,
+// rate constants, sparse change vectors) is staged once per CTA.  Per step: mass-action
+// propensities (R20) written to the row while reducing alpha_max / alpha_0
+// exactly as the matrix kernel does, tau, the first-accept trials of kernels_rows.cu,
+// then X += v_j and t += tau -- nothing leaves the SM until the run ends.  Realization
+// k is selection s0 + k and step i uses epoch epoch0 + i, so every step is bit-identical
+// to a gpuar_select on the same row.
+#include <algorithm>
+
+#include "gpuar_internal.cuh"
+#include "philox.cuh"
+
+namespace gpuar {
+
+namespace {
+
+// mass-action propensity, binary32 left to right (same operation order as the oracle)
+__device__ __forceinline__ float propensity(uint32_t xs, int32_t r0, int32_t r1, float c) {
+  float a = c;
+  if (r0 >= 0) {
+    const int32_t x0 = (int32_t)lds_u32(xs + 4u * (uint32_t)r0);
+    if (r1 == r0) {
+      if (x0 < 2) return 0.0f;
+      a = __fmul_rn(a, (float)x0);
+      a = __fmul_rn(a, (float)(x0 - 1));
+      return __fmul_rn(a, 0.5f);
+    }
+    a = __fmul_rn(a, (float)x0);
+  }
+  if (r1 >= 0) a = __fmul_rn(a, (float)(int32_t)lds_u32(xs + 4u * (uint32_t)r1));
+  return a;
+}
+
+template <bool FOLD>
+__device__ __forceinline__ void ssa_trials(const TrialStream& ts, uint32_t sel, uint32_t row_s, uint32_t M,
+                                           float amax, uint32_t half, uint32_t calls, uint32_t lane, int32_t& id) {
+  const float amax_s = __fmul_rn(amax, 0x1p-24f);
+  for (uint32_t c0 = 0; c0 < calls; c0 += 32u) {
+    const uint32_t c = c0 + lane;
+    const Philox4 x = ts(c, sel);
+    const uint32_t j0 = __umulhi(x.x, M);
+    const uint32_t j1 = __umulhi(x.z, M);
+    const float v0 = lds_f32(row_s + 4u * j0);
+    const float v1 = lds_f32(row_s + 4u * j1);
+    const bool a0 = (c < calls) & (scaled_u<FOLD>(x.y, amax, amax_s) < v0);
+    const bool a1 = (c < half) & (scaled_u<FOLD>(x.w, amax, amax_s) < v1);
+    const uint32_t b = __ballot_sync(kFull, a0 || a1);
+    if (b != 0u) {
+      id = (int32_t)__shfl_sync(kFull, a0 ? j0 : j1, __ffs(b) - 1);
+      return;
+    }
+  }
+}
+
+__global__ void __launch_bounds__(768, 1) ssa_kernel(const SsaParams P) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  const uint32_t warps = blockDim.x >> 5, warp = threadIdx.x >> 5, lane = threadIdx.x & 31u;
+  const uint32_t M = P.M, N = P.N, D = P.D;
+  // ---- stage the network: reac (M x 2), rate (M), didx / dval (M x D)
+  int32_t* s_reac = reinterpret_cast<int32_t*>(smem);
+  float* s_rate = reinterpret_cast<float*>(s_reac + 2u * M);
+  int32_t* s_didx = reinterpret_cast<int32_t*>(s_rate + M);
+  int32_t* s_dval = s_didx + D * M;
+  for (uint32_t i = threadIdx.x; i < 2u * M; i += blockDim.x) s_reac[i] = P.reac[i];
+  for (uint32_t i = threadIdx.x; i < M; i += blockDim.x) s_rate[i] = P.rate[i];
+  for (uint32_t i = threadIdx.x; i < D * M; i += blockDim.x) {
+    s_didx[i] = P.didx[i];
+    s_dval[i] = P.dval[i];
+  }
+  __syncthreads();
+  unsigned char* mine = smem + P.net_bytes + (size_t)warp * P.warp_bytes;
+  const uint32_t row_s = smem_u32(mine);
+  const uint32_t xs = row_s + ((4u * M + 15u) & ~15u);
+  int32_t* Xs = reinterpret_cast<int32_t*>(mine + ((4u * M + 15u) & ~15u));
+  float* row = reinterpret_cast<float*>(mine);
+
+  const uint32_t half = P.max_trials >> 1;
+  const uint32_t calls = half + (P.max_trials & 1u);
+  TrialStream ts(P.seed_lo, P.seed_hi, P.epoch0);
+  const uint32_t WT = gridDim.x * warps;
+  const uint32_t full_chunks = M >> 8;
+
+  for (uint32_t k = blockIdx.x * warps + warp; k < P.K; k += WT) {
+    int32_t* Xg = P.X + (size_t)k * N;
+    for (uint32_t i = lane; i < N; i += 32u) Xs[i] = Xg[i];
+    double t = P.t[k];
+    uint32_t fired = 0;
+    const uint32_t s = P.s0 + k;
+    __syncwarp();
+    for (int32_t step = 0; step < P.n_steps; ++step) {
+      // ---- propensities -> row, with alpha_max (bits) and alpha_0 as in kernels_rows.cu
+      uint32_t mx = 0;
+      double acc = 0.0;
+      for (uint32_t ch = 0; ch < full_chunks; ++ch) {
+        float v[8];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+          const uint32_t j = ch * 256u + (uint32_t)q * 32u + lane;
+          v[q] = propensity(xs, s_reac[2u * j], s_reac[2u * j + 1u], s_rate[j]);
+          row[j] = v[q];
+          mx = max(mx, __float_as_uint(v[q]));
+        }
+        acc += (double)__fadd_rn(__fadd_rn(__fadd_rn(v[0], v[1]), __fadd_rn(v[2], v[3])),
+                                 __fadd_rn(__fadd_rn(v[4], v[5]), __fadd_rn(v[6], v[7])));
+      }
+      {
+        float sum = 0.f;
+        for (uint32_t j = (full_chunks << 8) + lane; j < M; j += 32u) {
+          const float v = propensity(xs, s_reac[2u * j], s_reac[2u * j + 1u], s_rate[j]);
+          row[j] = v;
+          mx = max(mx, __float_as_uint(v));
+          sum = __fadd_rn(sum, v);
+        }
+        acc += (double)sum;
+      }
+      mx = __reduce_max_sync(kFull, mx);
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(kFull, acc, o);
+      __syncwarp();  // row complete before the gathers
+      if (mx >= kInfBits) {  // invalid propensity: sticky EPROPENSITY, stop this realization
+        if (lane == 0) atomicOr(&P.ctr->err, 1u);
+        break;
+      }
+      if (mx == 0u) break;  // nothing can fire: halted
+      const uint32_t epoch = P.epoch0 + (uint32_t)step;
+      const float tau = __fdiv_rn(neg_log_u1(P.seed_lo, P.seed_hi, s, epoch), __double2float_rn(acc));
+      if (t + (double)tau > P.t_end) break;  // the next event is past t_end
+      ts.set_epoch(epoch);
+      int32_t id = -1;
+      const float amax = __uint_as_float(mx);
+      if (can_fold(mx))
+        ssa_trials<true>(ts, ts.sel_word(s), row_s, M, amax, half, calls, lane, id);
+      else
+        ssa_trials<false>(ts, ts.sel_word(s), row_s, M, amax, half, calls, lane, id);
+      if (id >= 0) {  // X += v_id, t += tau  (rejected: no event this step, R21)
+        if (lane < D) {
+          const int32_t sp = s_didx[(uint32_t)id * D + lane];
+          if (sp >= 0) atomicAdd(&Xs[sp], s_dval[(uint32_t)id * D + lane]);
+        }
+        t += (double)tau;
+        ++fired;
+      }
+      __syncwarp();
+    }
+    __syncwarp();
+    for (uint32_t i = lane; i < N; i += 32u) Xg[i] = Xs[i];
+    if (lane == 0) {
+      P.t[k] = t;
+      if (P.steps) P.steps[k] = fired;
+    }
+    __syncwarp();
+  }
+}
+
+}  // namespace
+
+cudaError_t launch_ssa(const SsaParams& p, int grid, int warps, cudaStream_t st) {
+  const size_t sh = (size_t)p.net_bytes + (size_t)warps * p.warp_bytes;
+  ssa_kernel<<<grid, warps * 32, sh, st>>>(p);
+  return cudaGetLastError();
+}
+
+int ssa_blocks_per_sm(int warps, size_t smem) {
+  int n = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, ssa_kernel, warps * 32, smem) != cudaSuccess) return 0;
+  return n;
+}
+
+void set_ssa_limits(int bytes) {
+  cudaFuncSetAttribute(ssa_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+}
+
+}  // namespace gpuar

@@ -72,6 +72,13 @@ struct TrialStream {
     k1_tag = seed_hi ^ tag;
   }
 
+  // switch to another epoch (counter word 2) keeping the round keys
+  __device__ __forceinline__ void set_epoch(uint32_t epoch) {
+    const uint64_t p1 = (uint64_t)kPhiloxM1 * epoch;
+    e_hi_k0 = (uint32_t)(p1 >> 32) ^ rk0[0];
+    e_lo = (uint32_t)p1;
+  }
+
   // per-selection constant of round 1
   __device__ __forceinline__ uint32_t sel_word(uint32_t s) const { return e_hi_k0 ^ s; }
 

@@ -161,6 +161,29 @@ class Selector:
         self._rows = 0
         return idx, tau, trials
 
+    # ----------------------------------------------------------------- full SSA (NEXT-2)
+    def set_network(self, reac: torch.Tensor, rate: torch.Tensor, didx: torch.Tensor, dval: torch.Tensor,
+                    N: int) -> None:
+        """gpuar_set_network: mass-action network (cuda int32 reac (M,2), float32 rate (M,),
+        int32 didx/dval (M,D)); tensors are kept alive by the selector."""
+        D = didx.shape[1]
+        with torch.cuda.device(self.device):
+            check(self._lib.gpuar_set_network(self._h, int(N), int(D), _ptr(reac), _ptr(rate), _ptr(didx), _ptr(dval)),
+                  "gpuar_set_network")
+        self._net = (reac, rate, didx, dval)
+
+    def ssa_run(self, X: torch.Tensor, t: torch.Tensor, n_steps: int, t_end: float = float("inf"),
+                steps: torch.Tensor | None = None) -> torch.Tensor:
+        """gpuar_ssa_run: advance K realizations in place (X (K,N) int32, t (K,) float64)."""
+        K = X.shape[0]
+        if steps is None:
+            steps = torch.zeros(K, dtype=torch.int32, device=self.device)
+        with torch.cuda.device(self.device):
+            self._stream()
+            check(self._lib.gpuar_ssa_run(self._h, _ptr(X), _ptr(t), _ptr(steps), K, int(n_steps), float(t_end)),
+                  "gpuar_ssa_run")
+        return steps
+
     # ----------------------------------------------------------------- statistics / validation
     def stats(self) -> tuple[float, float, float]:
         amax, a0, p = ctypes.c_float(), ctypes.c_double(), ctypes.c_float()

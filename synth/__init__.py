@@ -118,3 +118,56 @@ def rows(rates: np.ndarray, gen_seed: int, k0: int, n: int, ld: int | None = Non
     out = np.zeros((n, ld), np.float32)
     out[:, :M] = np.where(bit, rates[None, :], np.float32(0.0))
     return out
+
+
+# ----------------------------------------------------------------- reaction networks (NEXT-2)
+# A network is a dict of int32/float32 arrays: reac (M,2) reactant species (-1 = none),
+# rate (M,) mass-action constants, didx/dval (M,D) sparse state-change vector v_j
+# (species -1 = unused slot).  Shapes only -- the propensity arithmetic is not here.
+
+def immigration_death(k: float = 10.0, gamma: float = 1.0) -> dict:
+    """0 -> X (rate k), X -> 0 (rate gamma X): X(t) ~ Poisson(k/gamma (1 - e^-gamma t)) from
+    X(0) = 0 (SPEC.md:418-419 uses the stationary mean 10)."""
+    return dict(reac=np.array([[-1, -1], [0, -1]], np.int32), rate=np.array([k, gamma], np.float32),
+                didx=np.array([[0], [0]], np.int32), dval=np.array([[1], [-1]], np.int32), N=1)
+
+
+def dimerisation(kf: float = 0.01, kb: float = 0.5) -> dict:
+    """2A -> B (rate kf A(A-1)/2), B -> 2A (rate kb B): A + 2B is conserved."""
+    return dict(reac=np.array([[0, 0], [1, -1]], np.int32), rate=np.array([kf, kb], np.float32),
+                didx=np.array([[0, 1], [0, 1]], np.int32), dval=np.array([[-2, 1], [2, -1]], np.int32), N=2)
+
+
+def yeast_like_network(N: int = 641, M: int = YEAST_M, gen_seed: int = GEN_SEED, D: int = 4) -> dict:
+    """A random mass-action network with the iron model's size (641 species, 1029 reactions,
+    PAPER.md:86-89; the model itself is unpublished): 15 % zeroth-order productions, 50 %
+    first-order (degradation or conversion), 35 % second-order (5 % of them dimerisations);
+    rates from yeast_rates, second-order ones scaled by 1e-2."""
+    rng = _rng(gen_seed + 7)
+    rates = yeast_rates(M, gen_seed).astype(np.float64)
+    reac = np.full((M, 2), -1, np.int32)
+    didx = np.full((M, D), -1, np.int32)
+    dval = np.zeros((M, D), np.int32)
+    for j in range(M):
+        order = rng.choice(3, p=[0.15, 0.50, 0.35])
+        if order >= 1:
+            reac[j, 0] = rng.integers(N)
+        if order == 2:
+            reac[j, 1] = reac[j, 0] if rng.random() < 0.05 else rng.integers(N)
+            rates[j] *= 1e-2
+        delta = {}
+        for r in reac[j]:
+            if r >= 0:
+                delta[int(r)] = delta.get(int(r), 0) - 1
+        for _ in range(rng.integers(0, 3) if order > 0 else 1):
+            sp = int(rng.integers(N))
+            delta[sp] = delta.get(sp, 0) + 1
+        items = [(sp, v) for sp, v in delta.items() if v != 0][:D]
+        for d, (sp, v) in enumerate(items):
+            didx[j, d], dval[j, d] = sp, v
+    return dict(reac=reac, rate=rates.astype(np.float32), didx=didx, dval=dval, N=N)
+
+
+def initial_state(N: int, K: int, gen_seed: int = GEN_SEED, high: int = 10) -> np.ndarray:
+    """K x N initial copy numbers, uniform on [0, high)."""
+    return _rng(gen_seed + 11).integers(0, high, size=(K, N), dtype=np.int32)
