@@ -120,10 +120,16 @@ int gpuar_select_host(gpuar_t h, const float *h_alpha, int64_t rows, int64_t ld,
  *     u_j = fl32(v_j T), eligible iff u_j < alpha_j with rating R_j = fl32(u_j / alpha_j),
  *     else R_j = 1; idx = argmin_j R_j (ties to the lowest j), -1 if min R >= 1; trials = M.
  *     Its law is NOT alpha_j / alpha_0 (R1).
- * Applies to later gpuar_select / gpuar_select_host calls (shared vector and matrix).
+ *   GPUAR_RULE_IT (w must be 1; shared vector only): the classic inverse transform, the
+ *     direct method the paper replaces: u2 = (x >> 8) 2^-24 from Philox
+ *     counter {0, s_g, epoch, 2}; idx = the smallest j with C_j > u2 * alpha_0, C_j the
+ *     sequential binary64 prefix sum (computed once per registered vector, O(M)); trials = 1.
+ * Applies to later gpuar_select / gpuar_select_host calls (shared vector and matrix; IT:
+ * gpuar_select on a matrix returns EINVAL).
  * Errors: EINVAL (unknown rule, w out of range). */
 #define GPUAR_RULE_CLASSIC 0
 #define GPUAR_RULE_ARGMIN  1
+#define GPUAR_RULE_IT      2
 int gpuar_set_rule(gpuar_t h, int rule, float w);
 
 /* NEXT-2: the full SSA loop around the selector.

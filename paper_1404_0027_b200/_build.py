@@ -21,7 +21,7 @@ NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-fmad=false", "-shared", "-Xcompiler", "-fPIC"]
 
-SOURCES = ["gpuar_api.cu", "kernels_misc.cu", "kernels_select.cu", "kernels_rows.cu", "kernels_argmin.cu", "kernels_ssa.cu"]
+SOURCES = ["gpuar_api.cu", "kernels_misc.cu", "kernels_select.cu", "kernels_rows.cu", "kernels_argmin.cu", "kernels_ssa.cu", "kernels_it.cu"]
 
 
 def _stale(target: str, deps: list[str]) -> bool:

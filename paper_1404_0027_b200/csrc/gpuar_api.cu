@@ -82,6 +82,9 @@ struct gpuar_handle {
   const int32_t* net_dval = nullptr;
   int64_t net_N = 0, net_D = 0;
   int ssa_warps = 0, ssa_grid = 0;
+  // inverse transform (GPUAR_RULE_IT): sequential binary64 prefix sums of the shared vector
+  double* d_prefix = nullptr;
+  bool prefix_valid = false;
   uint32_t ssa_net_bytes = 0, ssa_warp_bytes = 0;
   Chunked host;
 };
@@ -146,15 +149,15 @@ int plan_rows(gpuar_handle* h) {
   const uint64_t sb = ((4ull * (uint64_t)h->M + 15ull) & ~15ull) + 16ull;
   int W = env_int("GPUAR_ROWS_WARPS", kRowsDefaultWarps);
   W = std::max(1, std::min(W, kRowsMaxWarps));
-  int S = env_int("GPUAR_ROWS_STAGES", 0);
+  int S = env_int("GPUAR_ROWS_STAGES", 0);    // 1, 2 or 4 (powers of two: slot by shift)
   auto fits = [&](int w, int s) { return (((uint64_t)w * s * 8u + 127u) & ~127ull) + (uint64_t)w * s * sb <= budget; };
-  if (S <= 0) {
+  if (S != 1 && S != 2 && S != 4) {
     S = 4;
-    while (S > 2 && !fits(W, S)) --S;
+    while (S > 2 && !fits(W, S)) S >>= 1;
   }
   if (S > 1 && !fits(W, S) && W > 16) S = 1;   // many warps with no prefetch beat few with it
   while (W > 1 && !fits(W, S)) --W;
-  if (!fits(W, S) || S > 32) return GPUAR_EINVAL;  // M too large for the row pipeline
+  if (!fits(W, S)) return GPUAR_EINVAL;  // M too large for the row pipeline
   h->rows_warps = W;
   h->rows_stages = S;
   h->rows_lb = std::max(0, std::min(5, env_int("GPUAR_ROWS_LOG2_BLOCK", 2)));
@@ -189,9 +192,18 @@ int launch_select(gpuar_handle* h, const float* alpha, int64_t rows, int64_t ld,
     p.group_shift = h->group_shift;
     p.smem_bytes = h->shared_smem;
     p.w = h->w;
-    if (h->rule == kRuleArgmin)
+    if (h->rule == kRuleArgmin) {
       e = launch_argmin_shared(p, h->am_smem, h->am_grid, 256, st);
-    else
+    } else if (h->rule == kRuleIT) {
+      e = cudaSuccess;
+      if (!h->d_prefix) e = cudaMalloc(&h->d_prefix, sizeof(double) * (size_t)h->M);
+      if (e == cudaSuccess && !h->prefix_valid) {
+        e = launch_it_prefix(alpha, (uint32_t)h->M, h->d_prefix, st);
+        h->prefix_valid = e == cudaSuccess;
+      }
+      const bool smem = (size_t)h->M * 8u + 1024u <= (size_t)h->smem_optin;
+      if (e == cudaSuccess) e = launch_it_select(p, h->d_prefix, smem, h->num_sms * 8, st);
+    } else
       e = launch_select_shared(p, h->shared_path, h->sh_grid, h->sh_block, st);
   } else {
     RowsParams p{};
@@ -208,7 +220,7 @@ int launch_select(gpuar_handle* h, const float* alpha, int64_t rows, int64_t ld,
     p.seed_lo = (uint32_t)h->seed;
     p.seed_hi = (uint32_t)(h->seed >> 32);
     p.max_trials = h->max_trials;
-    p.stages = (uint32_t)h->rows_stages;
+    p.log2_stages = h->rows_stages == 4 ? 2u : (h->rows_stages == 2 ? 1u : 0u);
     p.stage_bytes = h->stage_bytes;
     p.stats_only = 0;
     p.rule = h->rule;
@@ -244,6 +256,7 @@ int register_shared(gpuar_handle* h, const float* d_alpha) {
   h->rows = 1;
   h->ld = h->M;
   h->path = h->shared_path;
+  h->prefix_valid = false;
   return GPUAR_OK;
 }
 
@@ -280,6 +293,7 @@ int gpuar_create(gpuar_t* out, int64_t M, int64_t K, uint64_t seed) {
   set_select_rows_limits(h->smem_optin);
   set_argmin_limits(h->smem_optin);
   set_ssa_limits(h->smem_optin);
+  set_it_limits(h->smem_optin);
   {
     const size_t am_sh = (size_t)((M + 3) & ~3ll) * 4u;
     h->am_smem = am_sh + 1024u <= (size_t)h->smem_optin;
@@ -327,6 +341,7 @@ int gpuar_destroy(gpuar_t h) {
   cudaFree(h->d_part_sum);
   cudaFree(h->d_part_max);
   cudaFree(h->d_pref);
+  cudaFree(h->d_prefix);
   delete h;
   return e == cudaSuccess ? GPUAR_OK : GPUAR_ECUDA;
 }
@@ -359,6 +374,7 @@ int gpuar_select(gpuar_t h, int64_t K, int32_t* d_idx, float* d_tau, uint32_t* d
   if (!h || !d_idx || K < 1 || K > h->Kcap) return GPUAR_EINVAL;
   if (h->path == kPathNone) return GPUAR_ENOTSET;
   if (h->rows != 1 && K != h->rows) return GPUAR_EINVAL;
+  if (h->rows != 1 && h->rule == kRuleIT) return GPUAR_EINVAL;  // IT: shared vector only
   if (h->offset + (uint64_t)K > (1ull << 32)) return GPUAR_EINVAL;
   DeviceGuard g(h->device);
   if (!g.ok) return GPUAR_ECUDA;
@@ -473,7 +489,7 @@ int gpuar_select_host(gpuar_t h, const float* h_alpha, int64_t rows, int64_t ld,
 
 int gpuar_set_rule(gpuar_t h, int rule, float w) {
   if (!h) return GPUAR_EINVAL;
-  if (rule == GPUAR_RULE_CLASSIC) {
+  if (rule == GPUAR_RULE_CLASSIC || rule == GPUAR_RULE_IT) {
     if (w != 1.0f) return GPUAR_EINVAL;
   } else if (rule == GPUAR_RULE_ARGMIN) {
     if (!(w >= 1.0f) || !std::isfinite(w)) return GPUAR_EINVAL;
@@ -490,8 +506,8 @@ int gpuar_set_network(gpuar_t h, int64_t N, int64_t D, const int32_t* d_reac, co
   if (!h || !d_reac || !d_rate || !d_didx || !d_dval || N < 1 || N > 0x7fffffffll || D < 1 || D > 32)
     return GPUAR_EINVAL;
   const uint64_t M = (uint64_t)h->M;
-  const uint64_t net = ((M * (8u + 4u + 8u * (uint64_t)D)) + 15u) & ~15ull;
-  const uint64_t per_warp = ((4u * M + 15u) & ~15ull) + ((4u * (uint64_t)N + 15u) & ~15ull);
+  const uint64_t net = ((M * (16u + 8u * (uint64_t)D)) + 15u) & ~15ull;  // int4 descriptors + didx/dval
+  const uint64_t per_warp = ((4u * M + 15u) & ~15ull) + ((4u * ((uint64_t)N + 1u) + 15u) & ~15ull);
   const uint64_t budget = (uint64_t)h->smem_optin - 1024u;
   if (net + per_warp > budget) return GPUAR_EINVAL;  // network + one realization must fit on chip
   int W = (int)std::min<uint64_t>(24, (budget - net) / per_warp);
@@ -605,7 +621,7 @@ int gpuar_row_stats(gpuar_t h, float* d_amax, double* d_a0) {
   p.M = (uint32_t)h->M;
   p.K = (uint32_t)h->rows;
   p.max_trials = h->max_trials;
-  p.stages = (uint32_t)h->rows_stages;
+  p.log2_stages = h->rows_stages == 4 ? 2u : (h->rows_stages == 2 ? 1u : 0u);
   p.stage_bytes = h->stage_bytes;
   p.stats_only = 1;
   p.log2_block = (uint32_t)h->rows_lb;

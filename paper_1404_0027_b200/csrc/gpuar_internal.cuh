@@ -40,6 +40,7 @@ enum Path : int {
 enum Rule : int {
   kRuleClassic = 0,  // classic AR, first accept (the north_star hot path)
   kRuleArgmin = 1,   // the paper's printed election + argmin selection
+  kRuleIT = 2,       // inverse transform, the classic direct method
 };
 
 struct SharedParams {
@@ -77,7 +78,7 @@ struct RowsParams {
   uint32_t epoch;
   uint32_t seed_lo, seed_hi;
   uint32_t max_trials;
-  uint32_t stages;           // ring depth per warp
+  uint32_t log2_stages;      // ring depth per warp = 2^log2_stages (1, 2 or 4)
   uint32_t stage_bytes;      // bytes per ring slot (multiple of 16)
   uint32_t stats_only;       // 1: gpuar_row_stats (no trials)
   int rule;                  // kRuleClassic / kRuleArgmin
@@ -104,8 +105,11 @@ struct SsaParams {
 
 // ---------------------------------------------------------------- PTX helpers
 // Shared-memory loads by 32-bit shared-window address (no generic->shared conversion per
-// access).  volatile + "memory": never hoisted above the barriers / bulk-copy waits /
-// stores that produce the data (ring slots and SSA rows are rewritten in place).
+// access).  volatile: never deleted, duplicated or merged (ring slots and SSA rows are
+// rewritten in place) and never reordered against the other side-effecting operations that
+// produce the data -- __syncthreads / __syncwarp, the mbarrier wait, the bulk-copy issue.
+// No "memory" clobber: it would force every kernel parameter to be re-read from the
+// constant bank after each load (LDCU traffic seen in r01_c4_select_rows_v6).
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
@@ -157,27 +161,44 @@ __device__ __forceinline__ void fence_proxy_async_smem() {
 
 __device__ __forceinline__ float lds_f32(uint32_t addr) {
   float v;
-  asm volatile("ld.shared.f32 %0, [%1];" : "=f"(v) : "r"(addr) : "memory");
+  asm volatile("ld.shared.f32 %0, [%1];" : "=f"(v) : "r"(addr));
   return v;
 }
 
 __device__ __forceinline__ float4 lds_f32x4(uint32_t addr) {
   float4 v;
-  asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(addr)
-               : "memory");
+  asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(addr));
+  return v;
+}
+
+__device__ __forceinline__ int4 lds_i4(uint32_t addr) {
+  int4 v;
+  asm volatile("ld.shared.v4.s32 {%0, %1, %2, %3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(addr));
   return v;
 }
 
 __device__ __forceinline__ uint32_t lds_u32(uint32_t addr) {
   uint32_t v;
-  asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(addr) : "memory");
+  asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(addr));
   return v;
 }
 
 __device__ __forceinline__ uint32_t lds_u16(uint32_t addr) {
   unsigned short v;
-  asm volatile("ld.shared.u16 %0, [%1];" : "=h"(v) : "r"(addr) : "memory");
+  asm volatile("ld.shared.u16 %0, [%1];" : "=h"(v) : "r"(addr));
   return v;
+}
+
+// Packed binary32 pair add (SASS FADD2, sm_100+): each half is one IEEE round-to-nearest add,
+// bit-identical to two __fadd_rn.
+__device__ __forceinline__ float2 fadd2_rn(float2 a, float2 b) {
+  unsigned long long ra, rb, rd;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(ra) : "f"(a.x), "f"(a.y));
+  asm("mov.b64 %0, {%1, %2};" : "=l"(rb) : "f"(b.x), "f"(b.y));
+  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(rd) : "l"(ra), "l"(rb));
+  float2 d;
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(d.x), "=f"(d.y) : "l"(rd));
+  return d;
 }
 
 __device__ __forceinline__ uint32_t lanemask_lt() {
@@ -195,6 +216,9 @@ cudaError_t launch_prefilter(const float* alpha, uint32_t M, uint16_t* pref, uin
 cudaError_t launch_select_shared(const SharedParams& p, int path, int grid, int block, cudaStream_t st);
 cudaError_t launch_argmin_shared(const SharedParams& p, bool smem, int grid, int block, cudaStream_t st);
 void set_argmin_limits(int bytes);
+cudaError_t launch_it_prefix(const float* alpha, uint32_t M, double* C, cudaStream_t st);
+cudaError_t launch_it_select(const SharedParams& p, const double* C, bool smem, int grid, cudaStream_t st);
+void set_it_limits(int bytes);
 cudaError_t launch_ssa(const SsaParams& p, int grid, int warps, cudaStream_t st);
 int ssa_blocks_per_sm(int warps, size_t smem);
 void set_ssa_limits(int bytes);

@@ -79,13 +79,17 @@ __device__ __forceinline__ void row_argmin(const TrialStream& ts, uint32_t sel, 
   id = (uint32_t)(best >> 32) < 0x3f800000u ? (int32_t)(uint32_t)best : -1;
 }
 
-template <int MAXW>
+// MODE: kRuleClassic / kRuleArgmin (selection), or kModeStats (gpuar_row_stats)
+constexpr int kModeStats = 2;
+
+template <int MAXW, int MODE>
 __global__ void __launch_bounds__(MAXW * 32, 1) select_rows_kernel(const RowsParams P) {
   extern __shared__ __align__(128) unsigned char smem[];
   const uint32_t warps = blockDim.x >> 5;
   const uint32_t warp = threadIdx.x >> 5;
   const uint32_t lane = threadIdx.x & 31u;
-  const uint32_t S = P.stages;
+  const uint32_t lS = P.log2_stages;  // ring depth S = 2^lS (1, 2 or 4): slot/parity by shifts
+  const uint32_t S = 1u << lS;
   const uint32_t SB = P.stage_bytes;
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem) + warp * S;
   unsigned char* ring = smem + ((warps * S * 8u + 127u) & ~127u) + (size_t)warp * S * SB;
@@ -108,8 +112,26 @@ __global__ void __launch_bounds__(MAXW * 32, 1) select_rows_kernel(const RowsPar
   const uint32_t lb = P.log2_block;
   const uint32_t bm = (1u << lb) - 1u;
   auto row_of = [&](uint32_t n) -> uint64_t { return ((((uint64_t)(n >> lb)) * WT + wg) << lb) + (n & bm); };
-  auto issue = [&](uint32_t n, uint32_t slot) {
-    const uint64_t off = row_of(n) * row_bytes;
+  // Incremental walk over this warp's rows (row index, byte offset, position in block): the
+  // per-row bookkeeping is two 64-bit adds instead of 64-bit products.
+  const uint64_t jump = (WT - 1u) * (bm + 1u) + 1u;  // from the last row of a block to the next block
+  const uint64_t jump_bytes = jump * row_bytes;
+  struct Walk {
+    uint64_t r, off;
+    uint32_t pos;
+  };
+  auto advance = [&](Walk& w) {
+    if (w.pos == bm) {
+      w.r += jump;
+      w.off += jump_bytes;
+      w.pos = 0;
+    } else {
+      w.r += 1u;
+      w.off += row_bytes;
+      w.pos += 1u;
+    }
+  };
+  auto issue = [&](uint64_t off, uint32_t slot) {
     const uint64_t a = off & ~15ull;
     const uint64_t e = (off + 4ull * M + 15ull) & ~15ull;
     const uint32_t bytes = (uint32_t)(e - a);
@@ -117,9 +139,11 @@ __global__ void __launch_bounds__(MAXW * 32, 1) select_rows_kernel(const RowsPar
     bulk_g2s(ring + (size_t)slot * SB, reinterpret_cast<const unsigned char*>(P.alpha) + a, bytes, &bars[slot],
              policy);
   };
-  if (lane == 0) {
-    for (uint32_t s = 0; s < S; ++s)
-      if (row_of(s) < K) issue(s, s);
+  Walk cur{wg << lb, (wg << lb) * row_bytes, 0u};
+  Walk pre = cur;  // row n + S: the next row to prefetch into the slot row n frees
+  for (uint32_t i = 0; i < S; ++i) {
+    if (lane == 0 && pre.r < K) issue(pre.off, i);
+    advance(pre);
   }
 
   const uint32_t half = P.max_trials >> 1;
@@ -132,42 +156,59 @@ __global__ void __launch_bounds__(MAXW * 32, 1) select_rows_kernel(const RowsPar
   float o_tau = 0.f;
   double o_a0 = 0.0;
 
-  for (uint32_t n = 0;; ++n) {
-    const uint64_t r = row_of(n);
-    if (r >= K) break;
-    const uint32_t slot = n % S;
-    const uint32_t parity = (n / S) & 1u;
-    if ((n & 31u) == 0u && !P.stats_only) {
+  for (uint32_t n = 0; cur.r < K; ++n) {
+    const uint64_t r = cur.r;
+    const uint32_t slot = n & (S - 1u);
+    const uint32_t parity = (n >> lS) & 1u;
+    if ((n & 31u) == 0u && MODE != kModeStats) {
       const uint64_t rr = row_of(n + lane);
       nlog = rr < K ? neg_log_u1(P.seed_lo, P.seed_hi, P.s0 + (uint32_t)rr, P.epoch) : 0.f;
     }
     mbar_wait(&bars[slot], parity);
     // The slot holds the row's 16-byte hull: element j sits at word lead + j.
-    const uint32_t lead = (uint32_t)((r * row_bytes) & 15ull) >> 2;
+    const uint32_t lead = (uint32_t)(cur.off & 15ull) >> 2;
     const uint32_t row_s = smem_u32(ring + (size_t)slot * SB) + 4u * lead;
 
-    // ---- alpha_max (max of bit patterns) and alpha_0: 8 scalar LDS per lane per chunk of
-    // 256 (conflict-free, consecutive lanes), pairwise binary32 sum of the 8 promoted to
-    // binary64.  (A 16-byte-vector variant with hull edge handling measured 3 % more
-    // instructions and 5 % slower: profiles/r01_c4_select_rows_v3.md.)
+    // ---- alpha_max (max of bit patterns) and alpha_0.  Each lane takes 16 elements per
+    // 512-chunk (conflict-free scalar LDS, consecutive lanes), sums them pairwise in binary32
+    // (depth 4, packed FADD2) and adds the chunk sum in binary64; a last 256-chunk likewise
+    // with 8, the < 256 tail sequentially (<= 8 per lane).  Relative error of alpha_0 before
+    // the final rounding <= 7u (R11).  (A 16-byte-vector variant measured slower:
+    // profiles/r01_c4_select_rows_v3.md.)
     uint32_t mx = 0;
     double acc = 0.0;
-    const uint32_t full_chunks = M >> 8;
-    for (uint32_t ch = 0; ch < full_chunks; ++ch) {
-      const uint32_t p = row_s + 4u * (ch * 256u + lane);
+    uint32_t base = 0;
+    for (; base + 512u <= M; base += 512u) {
+      const uint32_t p = row_s + 4u * (base + lane);
+      float v[16];
+#pragma unroll
+      for (int k = 0; k < 16; ++k) {
+        v[k] = lds_f32(p + 128u * k);
+        mx = max(mx, __float_as_uint(v[k]));
+      }
+      float2 q[8];
+#pragma unroll
+      for (int k = 0; k < 8; ++k) q[k] = make_float2(v[2 * k], v[2 * k + 1]);
+      const float2 r = fadd2_rn(fadd2_rn(fadd2_rn(q[0], q[1]), fadd2_rn(q[2], q[3])),
+                                fadd2_rn(fadd2_rn(q[4], q[5]), fadd2_rn(q[6], q[7])));
+      acc += (double)__fadd_rn(r.x, r.y);
+    }
+    if (base + 256u <= M) {
+      const uint32_t p = row_s + 4u * (base + lane);
       float v[8];
 #pragma unroll
       for (int k = 0; k < 8; ++k) {
         v[k] = lds_f32(p + 128u * k);
         mx = max(mx, __float_as_uint(v[k]));
       }
-      const float s = __fadd_rn(__fadd_rn(__fadd_rn(v[0], v[1]), __fadd_rn(v[2], v[3])),
-                                __fadd_rn(__fadd_rn(v[4], v[5]), __fadd_rn(v[6], v[7])));
-      acc += (double)s;
+      const float2 r = fadd2_rn(fadd2_rn(make_float2(v[0], v[1]), make_float2(v[2], v[3])),
+                                fadd2_rn(make_float2(v[4], v[5]), make_float2(v[6], v[7])));
+      acc += (double)__fadd_rn(r.x, r.y);
+      base += 256u;
     }
     {
-      float s = 0.f;  // tail: at most 8 elements per lane, sequential
-      for (uint32_t j = (full_chunks << 8) + lane; j < M; j += 32u) {
+      float s = 0.f;  // tail: < 256 elements, at most 8 per lane, sequential
+      for (uint32_t j = base + lane; j < M; j += 32u) {
         const float v = lds_f32(row_s + 4u * j);
         mx = max(mx, __float_as_uint(v));
         s = __fadd_rn(s, v);
@@ -178,8 +219,8 @@ __global__ void __launch_bounds__(MAXW * 32, 1) select_rows_kernel(const RowsPar
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(kFull, acc, o);
 
-    const uint32_t nl32 = n & bm;  // this row's slot in the block's output buffer
-    if (P.stats_only) {
+    const uint32_t nl32 = cur.pos;  // this row's slot in the block's output buffer
+    if constexpr (MODE == kModeStats) {
       if (lane == nl32) {
         o_tau = mx < kInfBits ? __uint_as_float(mx) : __uint_as_float(0x7fc00000u);
         o_a0 = mx < kInfBits ? acc : __longlong_as_double(0x7ff8000000000000ll);
@@ -198,7 +239,7 @@ __global__ void __launch_bounds__(MAXW * 32, 1) select_rows_kernel(const RowsPar
         const float amax = __uint_as_float(mx);
         tau = __fdiv_rn(nl, __double2float_rn(acc));
         const uint32_t sel = ts.sel_word(P.s0 + (uint32_t)r);
-        if (P.rule == kRuleArgmin) {
+        if constexpr (MODE == kRuleArgmin) {
           // the paper's printed rule on this row: election + argmin selection
           const float T = __fmul_rn(P.w, amax);
           if (can_fold(__float_as_uint(T)))
@@ -206,11 +247,13 @@ __global__ void __launch_bounds__(MAXW * 32, 1) select_rows_kernel(const RowsPar
           else
             row_argmin<false>(ts, sel, row_s, M, T, lane, id);
           tr = M;
-        } else if (can_fold(mx))
-          row_trials<true>(ts, sel, row_s, M, amax, half, calls, lane, id, tr);
-        else
-          row_trials<false>(ts, sel, row_s, M, amax, half, calls, lane, id, tr);
-        if (id < 0 && P.rule == kRuleClassic) tr = P.max_trials;
+        } else {
+          if (can_fold(mx))
+            row_trials<true>(ts, sel, row_s, M, amax, half, calls, lane, id, tr);
+          else
+            row_trials<false>(ts, sel, row_s, M, amax, half, calls, lane, id, tr);
+          if (id < 0) tr = P.max_trials;
+        }
       }
       if (lane == nl32) {
         o_id = id;
@@ -221,7 +264,7 @@ __global__ void __launch_bounds__(MAXW * 32, 1) select_rows_kernel(const RowsPar
     if (nl32 == bm || r + 1u >= K) {  // flush the block: one coalesced store per output
       const uint64_t rl = r - nl32 + lane;
       if (lane <= nl32) {
-        if (P.stats_only) {
+        if constexpr (MODE == kModeStats) {
           P.amax_out[rl] = o_tau;
           P.a0_out[rl] = o_a0;
         } else {
@@ -232,42 +275,59 @@ __global__ void __launch_bounds__(MAXW * 32, 1) select_rows_kernel(const RowsPar
       }
     }
     __syncwarp();
-    if (lane == 0 && row_of(n + S) < K) {
+    if (lane == 0 && pre.r < K) {
       fence_proxy_async_smem();  // generic-proxy reads of the slot precede the async refill
-      issue(n + S, slot);
+      issue(pre.off, slot);
     }
+    advance(cur);
+    advance(pre);
   }
+}
+
+template <int MAXW>
+cudaError_t launch_w(const RowsParams& p, int grid, int warps, size_t sh, cudaStream_t st) {
+  if (p.stats_only)
+    select_rows_kernel<MAXW, kModeStats><<<grid, warps * 32, sh, st>>>(p);
+  else if (p.rule == kRuleArgmin)
+    select_rows_kernel<MAXW, kRuleArgmin><<<grid, warps * 32, sh, st>>>(p);
+  else
+    select_rows_kernel<MAXW, kRuleClassic><<<grid, warps * 32, sh, st>>>(p);
+  return cudaGetLastError();
+}
+
+template <int MAXW>
+void set_limits_w(int bytes) {
+  cudaFuncSetAttribute(select_rows_kernel<MAXW, kRuleClassic>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+  cudaFuncSetAttribute(select_rows_kernel<MAXW, kRuleArgmin>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+  cudaFuncSetAttribute(select_rows_kernel<MAXW, kModeStats>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
 }
 
 }  // namespace
 
 cudaError_t launch_select_rows(const RowsParams& p, int grid, int warps, cudaStream_t st) {
-  const size_t sh = (((size_t)warps * p.stages * 8u + 127u) & ~(size_t)127u) + (size_t)warps * p.stages * p.stage_bytes;
-  if (warps <= 16)
-    select_rows_kernel<16><<<grid, warps * 32, sh, st>>>(p);
-  else if (warps <= 24)
-    select_rows_kernel<24><<<grid, warps * 32, sh, st>>>(p);
-  else
-    select_rows_kernel<32><<<grid, warps * 32, sh, st>>>(p);
-  return cudaGetLastError();
+  const size_t S = (size_t)1 << p.log2_stages;
+  const size_t sh = (((size_t)warps * S * 8u + 127u) & ~(size_t)127u) + (size_t)warps * S * p.stage_bytes;
+  if (warps <= 16) return launch_w<16>(p, grid, warps, sh, st);
+  if (warps <= 24) return launch_w<24>(p, grid, warps, sh, st);
+  return launch_w<32>(p, grid, warps, sh, st);
 }
 
 int select_rows_blocks_per_sm(int warps, size_t smem) {
   int n = 0;
   cudaError_t e;
   if (warps <= 16)
-    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, select_rows_kernel<16>, warps * 32, smem);
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, select_rows_kernel<16, kRuleClassic>, warps * 32, smem);
   else if (warps <= 24)
-    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, select_rows_kernel<24>, warps * 32, smem);
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, select_rows_kernel<24, kRuleClassic>, warps * 32, smem);
   else
-    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, select_rows_kernel<32>, warps * 32, smem);
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, select_rows_kernel<32, kRuleClassic>, warps * 32, smem);
   return e == cudaSuccess ? n : 0;
 }
 
 void set_select_rows_limits(int bytes) {
-  cudaFuncSetAttribute(select_rows_kernel<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
-  cudaFuncSetAttribute(select_rows_kernel<24>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
-  cudaFuncSetAttribute(select_rows_kernel<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+  set_limits_w<16>(bytes);
+  set_limits_w<24>(bytes);
+  set_limits_w<32>(bytes);
 }
 
 }  // namespace gpuar

@@ -208,15 +208,70 @@ __device__ __forceinline__ void trial_loop(const SharedParams& P, const TrialStr
   }
 }
 
-// Team size g (power of two, 1..32): minimise (waste in the last round ~ g p) +
-// (idle lanes while a warp's last selections drain ~ T ln T * warps / K, T = 32/g teams).
+// Whole-warp teams (g = 32): the warp works its selections one after another, 64 trials
+// per round, like the matrix kernel -- no per-round team bookkeeping, ~15 instructions of
+// overhead per selection (pool refill by lane 0 once per `grab` selections).
+template <int PATH, bool FOLD>
+__device__ __forceinline__ void warp_loop(const SharedParams& P, const TrialStream& ts, uint32_t sbase, float amax,
+                                          Pool pl) {
+  const float amax_s = __fmul_rn(amax, 0x1p-24f);
+  const uint32_t M = P.M;
+  const uint32_t half = P.max_trials >> 1;
+  const uint32_t calls = half + (P.max_trials & 1u);
+  const uint32_t lane = threadIdx.x & 31u;
+  while (!pl.exhausted) {
+    if (pl.next >= pl.end) {
+      unsigned long long b = 0;
+      if (lane == 0u) b = pl.dyn_base(pl.stripe) + atomicAdd(&P.ctr->next[pl.stripe], pl.grab);
+      b = __shfl_sync(kFull, b, 0);
+      const unsigned long long hi = pl.stripe_hi(pl.stripe);
+      if (b >= hi) break;
+      pl.next = b;
+      pl.end = min(b + pl.grab, hi);
+    }
+    const uint32_t my = (uint32_t)pl.next++;
+    const uint32_t sel = ts.sel_word(P.s0 + my);
+    int32_t id = -1;
+    uint32_t tr = P.max_trials;
+    for (uint32_t c0 = 0; c0 < calls; c0 += 32u) {
+      const uint32_t c = c0 + lane;
+      const Philox4 x = ts(c, sel);
+      const uint32_t j0 = __umulhi(x.x, M);
+      const uint32_t j1 = __umulhi(x.z, M);
+      const bool r0 = accept<PATH>(scaled_u<FOLD>(x.y, amax, amax_s), j0, sbase, P.alpha, P.group_shift);
+      const bool r1 = accept<PATH>(scaled_u<FOLD>(x.w, amax, amax_s), j1, sbase, P.alpha, P.group_shift);
+      const bool a0 = (c < calls) & r0;
+      const bool a1 = (c < half) & r1;
+      const uint32_t b = __ballot_sync(kFull, a0 || a1);
+      if (b != 0u) {
+        const uint32_t w = __ffs(b) - 1;
+        id = (int32_t)__shfl_sync(kFull, a0 ? j0 : j1, w);
+        tr = __shfl_sync(kFull, a0 ? 2u * c + 1u : 2u * c + 2u, w);
+        break;
+      }
+    }
+    if (lane == 0u) {
+      P.idx[my] = id;
+      if (P.trials) P.trials[my] = tr;
+    }
+  }
+}
+
+// Team size g (power of two, 1..32) minimising the estimated warp instructions per
+// selection (E = 1/p expected trials; SASS counts of the r01 build):
+//   g = 32 (warp_loop): (E/64 + 1/2) rounds x 62 + 15 per selection;
+//   g < 32 (trial_loop): (E + g)/64 warp-rounds x (67 + 55 P(any lane of the warp finished))
+// times (1 + drain tail), tail = T ln(T+1) * warps / K with T = 32/g teams per warp.
 __device__ __forceinline__ uint32_t choose_team(float p, uint32_t K, uint32_t nwarps) {
   const float wk = (float)nwarps / (float)max(K, 1u);
-  uint32_t best = 1u;
-  float best_cost = 3.0e38f;
-  for (uint32_t g = 1u; g <= 32u; g <<= 1) {
+  const float E = 1.0f / fmaxf(p, 1e-30f);
+  const float any = 1.0f - __expf(64.0f * __logf(fmaxf(1.0f - p, 1e-30f)));
+  uint32_t best = 32u;
+  float best_cost = (E / 64.0f + 0.5f) * 62.0f + 15.0f;
+  best_cost *= 1.0f + 0.6931f * wk;
+  for (uint32_t g = 1u; g < 32u; g <<= 1) {
     const float T = (float)(32u / g);
-    const float cost = (float)g * p + T * __logf(T + 1.0f) * wk;
+    const float cost = (E + (float)g) / 64.0f * (67.0f + 55.0f * any) * (1.0f + T * __logf(T + 1.0f) * wk);
     if (cost < best_cost) {
       best_cost = cost;
       best = g;
@@ -278,6 +333,11 @@ __global__ void __launch_bounds__(1024, 1) select_shared_kernel(const SharedPara
       trial_loop<PATH, true, false>(P, ts, sbase, amax, 1u, pl);
     else
       trial_loop<PATH, false, false>(P, ts, sbase, amax, 1u, pl);
+  } else if (g == 32u) {
+    if (fold)
+      warp_loop<PATH, true>(P, ts, sbase, amax, pl);
+    else
+      warp_loop<PATH, false>(P, ts, sbase, amax, pl);
   } else {
     if (fold)
       trial_loop<PATH, true, true>(P, ts, sbase, amax, g, pl);

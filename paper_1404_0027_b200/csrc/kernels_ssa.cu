@@ -20,21 +20,19 @@ namespace gpuar {
 
 namespace {
 
-// mass-action propensity, binary32 left to right (same operation order as the oracle)
-__device__ __forceinline__ float propensity(uint32_t xs, int32_t r0, int32_t r1, float c) {
-  float a = c;
-  if (r0 >= 0) {
-    const int32_t x0 = (int32_t)lds_u32(xs + 4u * (uint32_t)r0);
-    if (r1 == r0) {
-      if (x0 < 2) return 0.0f;
-      a = __fmul_rn(a, (float)x0);
-      a = __fmul_rn(a, (float)(x0 - 1));
-      return __fmul_rn(a, 0.5f);
-    }
-    a = __fmul_rn(a, (float)x0);
-  }
-  if (r1 >= 0) a = __fmul_rn(a, (float)(int32_t)lds_u32(xs + 4u * (uint32_t)r1));
-  return a;
+// Mass-action propensity, branch-free.  Per reaction a 16-byte descriptor {i0, i1, c, h}:
+// i0 = r0 (or N, a dummy species pinned at 1 in shared memory), i1 = r1 (or N for none and
+// for dimerisation), c = rate, h = 0.5 for dimerisation else 1.  Then
+//   a = ((c * x0) * x1) * h,  x1 = max(x0 - 1, 0) for dimerisation, X[i1] otherwise.
+// Multiplying by exactly 1.0 is the identity and c * 0 = +0, so this is bit-identical to
+// the oracle's branchy left-to-right definition (R20): order 0 -> c, order 1 ->
+// c x0, two species -> (c x0) x1, dimer -> ((c x)(x-1)) / 2 with +0 for x < 2.
+__device__ __forceinline__ float propensity(uint32_t xs, const int4 d) {
+  const int32_t x0 = (int32_t)lds_u32(xs + 4u * (uint32_t)d.x);
+  const int32_t xb = (int32_t)lds_u32(xs + 4u * (uint32_t)d.y);
+  const float h = __int_as_float(d.w);
+  const int32_t x1 = (h == 0.5f) ? max(x0 - 1, 0) : xb;
+  return __fmul_rn(__fmul_rn(__fmul_rn(__int_as_float(d.z), (float)x0), (float)x1), h);
 }
 
 template <bool FOLD>
@@ -62,18 +60,22 @@ __global__ void __launch_bounds__(768, 1) ssa_kernel(const SsaParams P) {
   extern __shared__ __align__(16) unsigned char smem[];
   const uint32_t warps = blockDim.x >> 5, warp = threadIdx.x >> 5, lane = threadIdx.x & 31u;
   const uint32_t M = P.M, N = P.N, D = P.D;
-  // ---- stage the network: reac (M x 2), rate (M), didx / dval (M x D)
-  int32_t* s_reac = reinterpret_cast<int32_t*>(smem);
-  float* s_rate = reinterpret_cast<float*>(s_reac + 2u * M);
-  int32_t* s_didx = reinterpret_cast<int32_t*>(s_rate + M);
+  // ---- stage the network: descriptors (M x int4), didx / dval (M x D)
+  int4* s_desc = reinterpret_cast<int4*>(smem);
+  int32_t* s_didx = reinterpret_cast<int32_t*>(s_desc + M);
   int32_t* s_dval = s_didx + D * M;
-  for (uint32_t i = threadIdx.x; i < 2u * M; i += blockDim.x) s_reac[i] = P.reac[i];
-  for (uint32_t i = threadIdx.x; i < M; i += blockDim.x) s_rate[i] = P.rate[i];
+  for (uint32_t j = threadIdx.x; j < M; j += blockDim.x) {
+    const int32_t r0 = P.reac[2u * j], r1 = P.reac[2u * j + 1u];
+    const bool dimer = r0 >= 0 && r1 == r0;
+    s_desc[j] = make_int4(r0 >= 0 ? r0 : (int32_t)N, (r1 >= 0 && !dimer) ? r1 : (int32_t)N,
+                          __float_as_int(P.rate[j]), __float_as_int(dimer ? 0.5f : 1.0f));
+  }
   for (uint32_t i = threadIdx.x; i < D * M; i += blockDim.x) {
     s_didx[i] = P.didx[i];
     s_dval[i] = P.dval[i];
   }
   __syncthreads();
+  const uint32_t desc_s = smem_u32(s_desc);
   unsigned char* mine = smem + P.net_bytes + (size_t)warp * P.warp_bytes;
   const uint32_t row_s = smem_u32(mine);
   const uint32_t xs = row_s + ((4u * M + 15u) & ~15u);
@@ -89,6 +91,7 @@ __global__ void __launch_bounds__(768, 1) ssa_kernel(const SsaParams P) {
   for (uint32_t k = blockIdx.x * warps + warp; k < P.K; k += WT) {
     int32_t* Xg = P.X + (size_t)k * N;
     for (uint32_t i = lane; i < N; i += 32u) Xs[i] = Xg[i];
+    if (lane == 0) Xs[N] = 1;  // dummy species: absent reactant
     double t = P.t[k];
     uint32_t fired = 0;
     const uint32_t s = P.s0 + k;
@@ -102,7 +105,7 @@ __global__ void __launch_bounds__(768, 1) ssa_kernel(const SsaParams P) {
 #pragma unroll
         for (int q = 0; q < 8; ++q) {
           const uint32_t j = ch * 256u + (uint32_t)q * 32u + lane;
-          v[q] = propensity(xs, s_reac[2u * j], s_reac[2u * j + 1u], s_rate[j]);
+          v[q] = propensity(xs, lds_i4(desc_s + 16u * j));
           row[j] = v[q];
           mx = max(mx, __float_as_uint(v[q]));
         }
@@ -112,7 +115,7 @@ __global__ void __launch_bounds__(768, 1) ssa_kernel(const SsaParams P) {
       {
         float sum = 0.f;
         for (uint32_t j = (full_chunks << 8) + lane; j < M; j += 32u) {
-          const float v = propensity(xs, s_reac[2u * j], s_reac[2u * j + 1u], s_rate[j]);
+          const float v = propensity(xs, lds_i4(desc_s + 16u * j));
           row[j] = v;
           mx = max(mx, __float_as_uint(v));
           sum = __fadd_rn(sum, v);

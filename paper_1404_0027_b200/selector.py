@@ -83,9 +83,10 @@ class Selector:
         check(self._lib.gpuar_set_selection_offset(self._h, int(s0)), "gpuar_set_selection_offset")
 
     def set_rule(self, rule: str = "classic", w: float = 1.0) -> None:
-        """gpuar_set_rule: "classic" (first accept, the hot path) or "argmin" (the paper's
-        printed election + argmin selection with threshold T = w * alpha_max)."""
-        code = {"classic": _abi.RULE_CLASSIC, "argmin": _abi.RULE_ARGMIN}[rule]
+        """gpuar_set_rule: "classic" (first accept, the hot path), "argmin" (the paper's
+        printed election + argmin selection with threshold T = w * alpha_max) or "it" (the
+        classic inverse transform, shared vector only)."""
+        code = {"classic": _abi.RULE_CLASSIC, "argmin": _abi.RULE_ARGMIN, "it": _abi.RULE_IT}[rule]
         check(self._lib.gpuar_set_rule(self._h, code, float(w)), "gpuar_set_rule")
 
     def set_max_trials(self, n: int) -> None:

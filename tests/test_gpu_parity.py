@@ -394,3 +394,39 @@ def test_set_rule_validation():
         sel.set_rule("classic", 2.0)
     with pytest.raises(GpuarError):
         sel.set_rule("argmin", 0.5)
+
+
+# ---------------------------------------------------------------- inverse transform (NEXT-3)
+
+@pytest.mark.parametrize("kind,M", [("hand", 4), ("yeast", 1029), ("exponential", 10_000), ("pareto", 100_000)])
+def test_it_shared_bit_exact(kind, M):
+    a = synth.hand([1, 2, 3, 4]) if kind == "hand" else synth.distribution(kind, M)
+    K = 50_000
+    sel = _sel(a.size, K)
+    sel.set_rule("it")
+    sel.set_selection_offset(11)
+    sel.epoch = 4
+    sel.set_propensities(torch.from_numpy(a).cuda())
+    idx, tau, trials = sel.select(K)
+    sel.sync()
+    ref = oracle.it_select(a, K, seed=SEED, epoch=4, s0=11, nthreads=8)
+    np.testing.assert_array_equal(idx.cpu().numpy(), ref)
+    tref = oracle.ar_select(a, K, seed=SEED, epoch=4, s0=11, max_trials=1, nthreads=8)["tau_ref"]
+    assert (np.abs(tau.cpu().numpy() - tref) / tref).max() <= TAU_RTOL
+    assert (trials.cpu() == 1).all()
+
+
+def test_it_law_and_rows_refused():
+    from paper_1404_0027_b200 import GpuarError
+    a = synth.hand([1, 2, 3, 4])
+    sel = _sel(4, 100_000)
+    sel.set_rule("it")
+    sel.set_propensities(torch.from_numpy(a).cuda())
+    idx, _, _ = sel.select(100_000)
+    h = np.bincount(idx.cpu().numpy(), minlength=4)
+    assert oracle.chi2_pvalue(h, oracle.exact_law(a))[1] > 0.001
+    sel2 = _sel(4, 8)
+    sel2.set_rule("it")
+    sel2.set_propensities(torch.ones((8, 4), device="cuda"))
+    with pytest.raises(GpuarError):
+        sel2.select(8)
