@@ -74,7 +74,7 @@ def parse():
     ap.add_argument("--K", type=int, default=None, help="selections per GPU")
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--max-trials", type=int, default=None, help="per-selection trial cap (default 2^20)")
-    ap.add_argument("--rule", default=None, choices=["classic", "argmin"])
+    ap.add_argument("--rule", default=None, choices=["classic", "argmin", "it"])
     ap.add_argument("--w", type=float, default=1.0, help="argmin rule threshold multiplier T = w alpha_max")
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
     ap.add_argument("--no-e2e", action="store_true")
