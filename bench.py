@@ -436,6 +436,23 @@ def run_gpuar(args, w, rank, world, local_rank):
     sel.close()
 
 
+def ssa_roofline(events_per_s: float) -> dict:
+    """Issue-slot roofline of the on-chip SSA loop: warp instructions per event from the
+    committed ncu capture of ssa_kernel x events/s, against 148 SM x 4 issue/clk x clock."""
+    p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    e = json.load(open(p)).get("s1") if os.path.exists(p) else None
+    mhz = float(measured_peaks().get("sm_max_mhz", 1965.0))
+    peak = SM_COUNT * 4 * mhz * 1e6 / 1e12
+    if not e:
+        return {"bound": "alu", "achieved": None, "peak": peak, "unit": "T warp-instr/s", "frac": None, "traffic": None}
+    ipe = e["warp_instructions_per_launch"] / e["events_per_launch"]
+    ach = events_per_s * ipe / 1e12
+    return {"bound": "alu", "achieved": ach, "peak": peak, "unit": "T warp-instr/s (issue slots)", "frac": ach / peak,
+            "traffic": None, "instructions_per_event": ipe, "source": e["report"],
+            "note": f"148 SM x 4 issue/clk x {mhz:.0f} MHz; per event: M mass-action propensities, "
+                    "alpha_max/a0, AR trials, state update, all on chip"}
+
+
 def run_ssa(args, w, rank, world, local_rank):
     """NEXT-2 workload: K realizations advance `inner` SSA steps per launch (gpuar_ssa_run)."""
     import torch
@@ -491,10 +508,7 @@ def run_ssa(args, w, rank, world, local_rank):
                "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
                "data": "synthetic (seeded synth/ network and initial state)",
                "config": {"workload": w["desc"], "M": M, "N": inp["N"], "K_per_gpu": K, "steps_per_launch": inner},
-               "roofline": {"bound": "alu", "achieved": value / 1e9, "peak": None, "unit": "G SSA events/s",
-                            "frac": None, "traffic": None,
-                            "note": "on-chip: per event M mass-action propensities + reductions + AR trials; "
-                                    "no HBM traffic but the state in/out per launch"},
+               "roofline": ssa_roofline(value),
                "cpu_baseline": cpu, "e2e": None, "gpu_launches": args.steps, "clocks": clk.summary(),
                "validation": {"events": events, "events_per_realization_per_launch": events / K / args.steps}}
         print(json.dumps(res), flush=True)

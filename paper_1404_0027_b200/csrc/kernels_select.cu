@@ -208,6 +208,68 @@ __device__ __forceinline__ void trial_loop(const SharedParams& P, const TrialStr
   }
 }
 
+// One lane per selection (g = 1, high p): every round each lane makes one Philox call for
+// its own selection; a lane that finishes stores its result and takes the next selection of
+// the warp's pool (one ballot + popc), with no cross-lane data exchange.
+template <int PATH, bool FOLD>
+__device__ __forceinline__ void lane_loop(const SharedParams& P, const TrialStream& ts, uint32_t sbase, float amax,
+                                          Pool pl) {
+  const float amax_s = __fmul_rn(amax, 0x1p-24f);
+  const uint32_t M = P.M;
+  const uint32_t half = P.max_trials >> 1;
+  const uint32_t calls = half + (P.max_trials & 1u);
+  const uint32_t lane = threadIdx.x & 31u;
+  const uint32_t lt = lanemask_lt();
+  uint32_t my = kNone, sel = 0, c = 0;
+  bool active = false;
+  uint32_t need = kFull;  // lanes without a selection
+  while (true) {
+    if (need != 0u) {  // warp-uniform: hand out selections
+      while (need != 0u && !pl.exhausted) {
+        if (pl.next >= pl.end) {
+          unsigned long long b = 0;
+          if (lane == 0u) b = pl.dyn_base(pl.stripe) + atomicAdd(&P.ctr->next[pl.stripe], pl.grab);
+          b = __shfl_sync(kFull, b, 0);
+          const unsigned long long hi = pl.stripe_hi(pl.stripe);
+          if (b >= hi) {
+            pl.exhausted = true;
+            break;
+          }
+          pl.next = b;
+          pl.end = min(b + pl.grab, hi);
+        }
+        const uint32_t avail = (uint32_t)(pl.end - pl.next);
+        const uint32_t r = __popc(need & lt);
+        const bool mine = ((need >> lane) & 1u) && r < avail;
+        if (mine) {
+          my = (uint32_t)pl.next + r;
+          sel = ts.sel_word(P.s0 + my);
+          c = 0;
+          active = true;
+        }
+        pl.next += min((uint32_t)__popc(need), avail);
+        need &= ~__ballot_sync(kFull, mine);
+      }
+      if (pl.exhausted && !__any_sync(kFull, active)) break;
+    }
+    const Philox4 x = ts(c, sel);
+    const uint32_t j0 = __umulhi(x.x, M);
+    const uint32_t j1 = __umulhi(x.z, M);
+    const bool r0 = accept<PATH>(scaled_u<FOLD>(x.y, amax, amax_s), j0, sbase, P.alpha, P.group_shift);
+    const bool r1 = accept<PATH>(scaled_u<FOLD>(x.w, amax, amax_s), j1, sbase, P.alpha, P.group_shift);
+    const bool a0 = (c < calls) & r0;
+    const bool a1 = (c < half) & r1;
+    const bool done = active & (a0 | a1 | (c + 1u >= calls));
+    if (done) {
+      P.idx[my] = a0 ? (int32_t)j0 : (a1 ? (int32_t)j1 : -1);
+      if (P.trials) P.trials[my] = a0 ? 2u * c + 1u : (a1 ? 2u * c + 2u : P.max_trials);
+      active = false;
+    }
+    ++c;
+    need = __ballot_sync(kFull, !active);
+  }
+}
+
 // Whole-warp teams (g = 32): the warp works its selections one after another, 64 trials
 // per round, like the matrix kernel -- no per-round team bookkeeping, ~15 instructions of
 // overhead per selection (pool refill by lane 0 once per `grab` selections).
@@ -260,7 +322,8 @@ __device__ __forceinline__ void warp_loop(const SharedParams& P, const TrialStre
 // Team size g (power of two, 1..32) minimising the estimated warp instructions per
 // selection (E = 1/p expected trials; SASS counts of the r01 build):
 //   g = 32 (warp_loop): (E/64 + 1/2) rounds x 62 + 15 per selection;
-//   g < 32 (trial_loop): (E + g)/64 warp-rounds x (67 + 55 P(any lane of the warp finished))
+//   g = 1 (lane_loop): (E + 1)/64 warp-rounds x (72 + 15 P(any lane of the warp finished));
+//   1 < g < 32 (trial_loop): (E + g)/64 warp-rounds x (67 + 55 P(any lane finished));
 // times (1 + drain tail), tail = T ln(T+1) * warps / K with T = 32/g teams per warp.
 __device__ __forceinline__ uint32_t choose_team(float p, uint32_t K, uint32_t nwarps) {
   const float wk = (float)nwarps / (float)max(K, 1u);
@@ -271,7 +334,8 @@ __device__ __forceinline__ uint32_t choose_team(float p, uint32_t K, uint32_t nw
   best_cost *= 1.0f + 0.6931f * wk;
   for (uint32_t g = 1u; g < 32u; g <<= 1) {
     const float T = (float)(32u / g);
-    const float cost = (E + (float)g) / 64.0f * (67.0f + 55.0f * any) * (1.0f + T * __logf(T + 1.0f) * wk);
+    const float round = (g == 1u) ? 72.0f + 15.0f * any : 67.0f + 55.0f * any;
+    const float cost = (E + (float)g) / 64.0f * round * (1.0f + T * __logf(T + 1.0f) * wk);
     if (cost < best_cost) {
       best_cost = cost;
       best = g;
@@ -317,7 +381,10 @@ __global__ void __launch_bounds__(1024, 1) select_shared_kernel(const SharedPara
   const uint32_t K = P.K;
   const uint32_t nwarps = nthreads >> 5;
   const uint32_t warp_global = tid >> 5;
-  const uint32_t g = choose_team(st.p, K, nwarps);
+  __shared__ uint32_t s_g;
+  if (threadIdx.x == 0) s_g = choose_team(st.p, K, nwarps);  // once per CTA, not per warp
+  __syncthreads();
+  const uint32_t g = s_g;
   // static first chunk: half of a warp's fair share; then grabs of ~8192 expected trials
   // (st.grab), at most an eighth of the fair share, at least one selection per team.
   const unsigned long long teams = 32u / g;
@@ -330,9 +397,9 @@ __global__ void __launch_bounds__(1024, 1) select_shared_kernel(const SharedPara
   const bool fold = can_fold(st.amax_bits);
   if (g == 1u) {
     if (fold)
-      trial_loop<PATH, true, false>(P, ts, sbase, amax, 1u, pl);
+      lane_loop<PATH, true>(P, ts, sbase, amax, pl);
     else
-      trial_loop<PATH, false, false>(P, ts, sbase, amax, 1u, pl);
+      lane_loop<PATH, false>(P, ts, sbase, amax, pl);
   } else if (g == 32u) {
     if (fold)
       warp_loop<PATH, true>(P, ts, sbase, amax, pl);

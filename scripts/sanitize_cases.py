@@ -1,0 +1,78 @@
+"""Small invocations of every libgpuar kernel, for compute-sanitizer (memcheck / racecheck /
+synccheck / initcheck).  Exits non-zero if any result differs from the oracle."""
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+
+import oracle  # noqa: E402
+import synth  # noqa: E402
+from paper_1404_0027_b200 import Selector  # noqa: E402
+
+SEED = 7
+
+
+def check(a, b, what):
+    if not np.array_equal(a, b):
+        print("MISMATCH", what)
+        sys.exit(1)
+
+
+def main():
+    # shared vector, all three smem paths + argmin + IT
+    for a in (synth.yeast_like(), synth.exponential(70_000), synth.pareto(300_000)):
+        K = 3000
+        sel = Selector(a.size, K, SEED)
+        sel.set_propensities(torch.from_numpy(a).cuda())
+        idx, tau, tr = sel.select(K)
+        sel.sync()
+        check(idx.cpu().numpy(), oracle.ar_select(a, K, seed=SEED, nthreads=8)["idx"], f"shared {sel.path}")
+        hist, tot = sel.histogram(idx, tr)
+        sel.set_rule("argmin", 1.5)
+        idx, _, _ = sel.select(K)
+        sel.sync()
+        check(idx.cpu().numpy(), oracle.argmin_select(a, K, seed=SEED, w=1.5, epoch=1, nthreads=8)["idx"], "argmin")
+        sel.set_rule("it")
+        idx, _, _ = sel.select(K)
+        sel.sync()
+        check(idx.cpu().numpy(), oracle.it_select(a, K, seed=SEED, epoch=2, nthreads=8), "it")
+    # rows (odd M: misaligned rows), stats, argmin rows
+    M, K = 1029, 700
+    host = synth.rows(synth.yeast_rates(M), synth.GEN_SEED, 0, K)
+    sel = Selector(M, K, SEED)
+    sel.set_propensities(torch.from_numpy(host).cuda())
+    idx, tau, tr = sel.select(K)
+    amax, a0 = sel.row_stats()
+    sel.sync()
+    check(idx.cpu().numpy(), oracle.ar_select(host, K, seed=SEED, nthreads=8)["idx"], "rows")
+    sel.set_rule("argmin", 1.0)
+    idx, _, _ = sel.select(K)
+    sel.sync()
+    check(idx.cpu().numpy(), oracle.argmin_select(host, K, seed=SEED, epoch=1, nthreads=8)["idx"], "rows argmin")
+    # host pipeline
+    sel = Selector(M, K, SEED)
+    hi, _, _ = sel.select_host(torch.from_numpy(host).pin_memory())
+    check(hi.numpy(), oracle.ar_select(host, K, seed=SEED, nthreads=8)["idx"], "select_host")
+    # SSA
+    net = synth.yeast_like_network()
+    X0 = synth.initial_state(641, 100)
+    sel = Selector(net["rate"].size, 100, SEED)
+    dev = {k: torch.from_numpy(np.ascontiguousarray(net[k])).cuda() for k in ("reac", "rate", "didx", "dval")}
+    sel.set_network(dev["reac"], dev["rate"], dev["didx"], dev["dval"], net["N"])
+    X = torch.from_numpy(X0).cuda()
+    t = torch.zeros(100, dtype=torch.float64, device="cuda")
+    sel.ssa_run(X, t, 10)
+    sel.sync()
+    check(X.cpu().numpy(), oracle.ssa_run(net, X0, np.zeros(100), 10, seed=SEED)["X"], "ssa")
+    # Philox microkernel
+    sink = torch.zeros(4096, dtype=torch.int32, device="cuda")
+    sel.bench_philox(4096, 4, sink)
+    sel.sync()
+    print("sanitize cases ok")
+
+
+if __name__ == "__main__":
+    main()

@@ -430,3 +430,57 @@ def test_it_law_and_rows_refused():
     sel2.set_propensities(torch.ones((8, 4), device="cuda"))
     with pytest.raises(GpuarError):
         sel2.select(8)
+
+
+# ---------------------------------------------------------------- full-size shared-vector configs
+
+def _sampled_rows(K):
+    return np.unique(np.concatenate([np.arange(2048), np.arange(K - 2048, K), np.arange(0, K, 997)]))
+
+
+def _check_sampled(a, K, rows, gi, gtr, gt, max_trials=1 << 20):
+    splits = np.nonzero(np.diff(rows) != 1)[0] + 1
+    for run in np.split(rows, splits):
+        ref = oracle.ar_select(a, run.size, seed=SEED, s0=int(run[0]), max_trials=max_trials, nthreads=8)
+        np.testing.assert_array_equal(gi[run], ref["idx"])
+        np.testing.assert_array_equal(gtr[run], ref["trials"])
+        rel = np.abs(gt[run] - ref["tau_ref"]) / ref["tau_ref"]
+        assert rel.max() <= TAU_RTOL
+
+
+@pytest.mark.slow
+@pytest.mark.parametrize("kind,M", [("uniform", 10_000), ("exponential", 100_000), ("pareto", 10_000)])
+def test_c3_full_size_sampled(kind, M):
+    """c3 cells at the bench's K = 2^20 (same launch configuration), oracle on sampled selections."""
+    a = synth.distribution(kind, M)
+    K = 1 << 20
+    sel = _sel(M, K)
+    sel.set_propensities(torch.from_numpy(a).cuda())
+    idx, tau, trials = sel.select(K)
+    sel.sync()
+    gi, gt, gtr = idx.cpu().numpy(), tau.cpu().numpy(), trials.cpu().numpy().view(np.uint32)
+    _check_sampled(a, K, _sampled_rows(K), gi, gtr, gt)
+    # every selection: a positive-propensity reaction, trials >= 1
+    assert (gi >= 0).all() and (a[gi] > 0).all() and (gtr >= 1).all()
+    p = oracle.acceptance_rate(a)
+    assert abs(gtr.mean() - 1 / p) < 5 * math.sqrt((1 - p) / K) / p
+
+
+@pytest.mark.slow
+def test_c5_full_size_sampled():
+    """c5 (M = 10^6 Pareto, group-max prefilter path) at the bench's K = 2^21 per GPU with the
+    bench's max_trials = 2^24; oracle on a sampled subset (first/last 2048 + every 9973rd)."""
+    a = synth.pareto(1_000_000)
+    K = 1 << 21
+    sel = _sel(a.size, K)
+    sel.set_max_trials(1 << 24)
+    sel.set_propensities(torch.from_numpy(a).cuda())
+    assert sel.path == "smem_group_max"
+    idx, tau, trials = sel.select(K)
+    sel.sync()
+    gi, gt, gtr = idx.cpu().numpy(), tau.cpu().numpy(), trials.cpu().numpy().view(np.uint32)
+    rows = np.unique(np.concatenate([np.arange(256), np.arange(K - 256, K), np.arange(0, K, 9973)]))
+    _check_sampled(a, K, rows, gi, gtr, gt, max_trials=1 << 24)
+    assert (gi >= 0).all() and (a[gi] > 0).all()
+    p = oracle.acceptance_rate(a)
+    assert abs(gtr.astype(np.float64).mean() - 1 / p) < 5 * math.sqrt((1 - p) / K) / p
