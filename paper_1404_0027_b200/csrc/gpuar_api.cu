@@ -113,23 +113,24 @@ int cuda_status(cudaError_t e) {
 void plan_shared(gpuar_handle* h) {
   const uint64_t budget = (uint64_t)h->smem_optin - 1024u;
   const uint64_t M = (uint64_t)h->M;
-  if (4u * M <= budget) {
+  // staged by a bulk copy of the 16-byte hull: up to 16 bytes of slack
+  if (4u * M + 16u <= budget) {
     h->shared_path = kPathSmemF32;
     h->n_pref = 0;
     h->group_shift = 0;
-    h->shared_smem = (uint32_t)((4u * M + 15u) & ~15ull);
-  } else if (2u * M <= budget) {
+    h->shared_smem = (uint32_t)(((4u * M + 15u) & ~15ull) + 16u);
+  } else if (2u * M + 16u <= budget) {
     h->shared_path = kPathSmemBf16;
     h->n_pref = (uint32_t)M;
     h->group_shift = 0;
-    h->shared_smem = (uint32_t)((2u * M + 15u) & ~15ull);
+    h->shared_smem = (uint32_t)(((2u * M + 15u) & ~15ull) + 16u);
   } else {
     uint32_t s = 1;
-    while (2u * ((M + (1ull << s) - 1) >> s) > budget) ++s;
+    while (2u * ((M + (1ull << s) - 1) >> s) + 16u > budget) ++s;
     h->shared_path = kPathSmemGroup;
     h->group_shift = s;
     h->n_pref = (uint32_t)((M + (1ull << s) - 1) >> s);
-    h->shared_smem = (uint32_t)((2u * h->n_pref + 15u) & ~15ull);
+    h->shared_smem = (uint32_t)(((2u * h->n_pref + 15u) & ~15ull) + 16u);
   }
   // block size maximising resident threads per SM
   int best_threads = 0;
@@ -196,7 +197,7 @@ int launch_select(gpuar_handle* h, const float* alpha, int64_t rows, int64_t ld,
       e = launch_argmin_shared(p, h->am_smem, h->am_grid, 256, st);
     } else if (h->rule == kRuleIT) {
       e = cudaSuccess;
-      if (!h->d_prefix) e = cudaMalloc(&h->d_prefix, sizeof(double) * (size_t)h->M);
+      if (!h->d_prefix) e = cudaMalloc(&h->d_prefix, (sizeof(double) * (size_t)h->M + 15u) & ~(size_t)15);
       if (e == cudaSuccess && !h->prefix_valid) {
         e = launch_it_prefix(alpha, (uint32_t)h->M, h->d_prefix, st);
         h->prefix_valid = e == cudaSuccess;
@@ -306,7 +307,7 @@ int gpuar_create(gpuar_t* out, int64_t M, int64_t K, uint64_t seed) {
   if (e == cudaSuccess) e = cudaMalloc(&h->d_ctr, sizeof(DevCounters));
   if (e == cudaSuccess) e = cudaMalloc(&h->d_part_sum, sizeof(double) * h->stats_blocks);
   if (e == cudaSuccess) e = cudaMalloc(&h->d_part_max, sizeof(uint32_t) * h->stats_blocks);
-  if (e == cudaSuccess && h->n_pref) e = cudaMalloc(&h->d_pref, sizeof(uint16_t) * h->n_pref);
+  if (e == cudaSuccess && h->n_pref) e = cudaMalloc(&h->d_pref, (sizeof(uint16_t) * h->n_pref + 15u) & ~(size_t)15);
   if (e == cudaSuccess) e = cudaMemset(h->d_ctr, 0, sizeof(DevCounters));
   if (e == cudaSuccess) e = cudaMemset(h->d_stats, 0, sizeof(DevStats));
   if (e == cudaSuccess) e = cudaDeviceSynchronize();

@@ -155,6 +155,35 @@ __device__ __forceinline__ uint64_t policy_evict_first() {
   return pol;
 }
 
+// 1-D bulk async copy without an L2 policy (data re-read by every CTA: keep it in L2).
+__device__ __forceinline__ void bulk_g2s_plain(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   smem_u32(dst)),
+               "l"(src), "r"(bytes), "r"(smem_u32(bar))
+               : "memory");
+}
+
+// Stage `nbytes` at global `src` into this CTA's shared memory at `dst` (16-byte aligned)
+// with bulk async copies of the 16-byte-aligned hull; returns the shared address of the
+// first byte of src.  Every thread of the CTA must call it (it synchronises the CTA).
+__device__ __forceinline__ uint32_t stage_to_smem(unsigned char* dst, const void* src, uint32_t nbytes, uint64_t* bar) {
+  const uintptr_t a = reinterpret_cast<uintptr_t>(src);
+  const uintptr_t lo = a & ~(uintptr_t)15;
+  const uint32_t total = (uint32_t)(((a + nbytes + 15u) & ~(uintptr_t)15) - lo);
+  if (threadIdx.x == 0) {
+    mbar_init(bar, 1u);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    mbar_arrive_expect_tx(bar, total);
+    for (uint32_t off = 0; off < total; off += 32768u)
+      bulk_g2s_plain(dst + off, reinterpret_cast<const unsigned char*>(lo) + off, min(32768u, total - off), bar);
+  }
+  mbar_wait(bar, 0u);
+  return smem_u32(dst) + (uint32_t)(a - lo);
+}
+
 __device__ __forceinline__ void fence_proxy_async_smem() {
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
 }
@@ -228,6 +257,15 @@ cudaError_t launch_histogram(const int32_t* idx, const uint32_t* trials, uint32_
                              cudaStream_t st);
 cudaError_t launch_bench_philox(uint32_t n_threads, uint32_t calls, uint32_t seed_lo, uint32_t seed_hi,
                                 uint32_t* sink, cudaStream_t st);
+
+// Allow `fn` the opt-in dynamic shared memory `optin` minus its own static shared memory
+// (asking for more than that is an error and would leave the 48 KB default in place).
+template <typename F>
+inline void set_max_dynamic_smem(F fn, int optin) {
+  cudaFuncAttributes a{};
+  if (cudaFuncGetAttributes(&a, fn) != cudaSuccess) return;
+  cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, optin - (int)a.sharedSizeBytes);
+}
 
 // Occupancy helpers (filled by the TU owning each kernel).
 int select_shared_blocks_per_sm(int path, int block, size_t smem);

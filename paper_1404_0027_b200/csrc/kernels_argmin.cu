@@ -95,7 +95,7 @@ __global__ void __launch_bounds__(256) argmin_shared_kernel(const SharedParams P
     }
   }
   if (invalid || zero) return;
-  if constexpr (SMEM) {
+  if constexpr (SMEM) {  // zero-padded to a multiple of 4 (LDS.128 per Philox call)
     float* sv = reinterpret_cast<float*>(smem);
     const uint32_t padded = (P.M + 3u) & ~3u;
     for (uint32_t j = threadIdx.x; j < padded; j += blockDim.x) sv[j] = j < P.M ? __ldg(P.alpha + j) : 0.f;
@@ -124,7 +124,7 @@ cudaError_t launch_argmin_shared(const SharedParams& p, bool smem, int grid, int
 }
 
 void set_argmin_limits(int bytes) {
-  cudaFuncSetAttribute(argmin_shared_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+  set_max_dynamic_smem(argmin_shared_kernel<true>, bytes);
 }
 
 }  // namespace gpuar

@@ -34,10 +34,9 @@ __global__ void __launch_bounds__(256) it_select_kernel(const SharedParams P, co
   extern __shared__ __align__(16) unsigned char smem[];
   const double* C = Cg;
   if constexpr (SMEM) {
-    double* Cs = reinterpret_cast<double*>(smem);
-    for (uint32_t j = threadIdx.x; j < P.M; j += blockDim.x) Cs[j] = Cg[j];
-    __syncthreads();
-    C = Cs;
+    __shared__ uint64_t stage_bar;
+    stage_to_smem(smem, Cg, 8u * P.M, &stage_bar);  // d_prefix is 256-byte aligned: no offset
+    C = reinterpret_cast<const double*>(smem);
   }
   const DevStats st = *P.stats;
   const bool invalid = st.valid == 0u;
@@ -80,14 +79,14 @@ cudaError_t launch_it_prefix(const float* alpha, uint32_t M, double* C, cudaStre
 
 cudaError_t launch_it_select(const SharedParams& p, const double* C, bool smem, int grid, cudaStream_t st) {
   if (smem)
-    it_select_kernel<true><<<grid, 256, (size_t)p.M * 8u, st>>>(p, C);
+    it_select_kernel<true><<<grid, 256, ((size_t)p.M * 8u + 15u) & ~(size_t)15, st>>>(p, C);
   else
     it_select_kernel<false><<<grid, 256, 0, st>>>(p, C);
   return cudaGetLastError();
 }
 
 void set_it_limits(int bytes) {
-  cudaFuncSetAttribute(it_select_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+  set_max_dynamic_smem(it_select_kernel<true>, bytes);
 }
 
 }  // namespace gpuar

@@ -297,9 +297,9 @@ cudaError_t launch_w(const RowsParams& p, int grid, int warps, size_t sh, cudaSt
 
 template <int MAXW>
 void set_limits_w(int bytes) {
-  cudaFuncSetAttribute(select_rows_kernel<MAXW, kRuleClassic>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
-  cudaFuncSetAttribute(select_rows_kernel<MAXW, kRuleArgmin>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
-  cudaFuncSetAttribute(select_rows_kernel<MAXW, kModeStats>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+  set_max_dynamic_smem(select_rows_kernel<MAXW, kRuleClassic>, bytes);
+  set_max_dynamic_smem(select_rows_kernel<MAXW, kRuleArgmin>, bytes);
+  set_max_dynamic_smem(select_rows_kernel<MAXW, kModeStats>, bytes);
 }
 
 }  // namespace

@@ -365,16 +365,11 @@ __global__ void __launch_bounds__(1024, 1) select_shared_kernel(const SharedPara
   }
   if (invalid || zero) return;  // uniform over the grid; the pool counter is untouched
 
-  // ---- phase B: stage the vector (path 1) or its prefilter (paths 2, 3) in smem
-  if constexpr (PATH == kPathSmemF32) {
-    float* sv = reinterpret_cast<float*>(smem);
-    for (uint32_t j = threadIdx.x; j < P.M; j += blockDim.x) sv[j] = __ldg(P.alpha + j);
-  } else {
-    uint16_t* pf = reinterpret_cast<uint16_t*>(smem);
-    for (uint32_t i = threadIdx.x; i < P.n_pref; i += blockDim.x) pf[i] = __ldg(P.prefilter + i);
-  }
-  __syncthreads();
-  const uint32_t sbase = smem_u32(smem);
+  // ---- phase B: stage the vector (path 1) or its prefilter (paths 2, 3) in smem with one
+  // bulk async copy per CTA (16-byte hull; the data starts `sbase` bytes into it)
+  __shared__ uint64_t stage_bar;
+  const uint32_t sbase = (PATH == kPathSmemF32) ? stage_to_smem(smem, P.alpha, 4u * P.M, &stage_bar)
+                                                : stage_to_smem(smem, P.prefilter, 2u * P.n_pref, &stage_bar);
 
   // ---- phase C: trials
   const float amax = __uint_as_float(st.amax_bits);
@@ -427,7 +422,7 @@ __global__ void __launch_bounds__(1024, 1) select_shared_kernel(const SharedPara
 
 template <int PATH>
 void set_limit(int bytes) {
-  cudaFuncSetAttribute(select_shared_kernel<PATH>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+  set_max_dynamic_smem(select_shared_kernel<PATH>, bytes);
 }
 
 }  // namespace

@@ -176,7 +176,7 @@ int ssa_blocks_per_sm(int warps, size_t smem) {
 }
 
 void set_ssa_limits(int bytes) {
-  cudaFuncSetAttribute(ssa_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+  set_max_dynamic_smem(ssa_kernel, bytes);
 }
 
 }  // namespace gpuar
