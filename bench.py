@@ -363,9 +363,21 @@ def run_gpuar(args, w, rank, world, local_rank):
         achieved = bytes_per_launch / (ms_step * 1e-3) / 1e9
         peak = float(peaks["hbm_gbs"])
         traffic = ncu_traffic(args.config)
+        # diagnostic: the same row pipeline streaming the matrix with only the alpha_max /
+        # alpha_0 reduction (gpuar_row_stats, no trials) -- what the pipeline itself can read
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        sel.row_stats()
+        n_rs = 20
+        e0.record(stream)
+        for _ in range(n_rs):
+            sel.row_stats()
+        e1.record(stream)
+        e1.synchronize()
+        rs_gbs = K * 4 * M / (e0.elapsed_time(e1) / n_rs * 1e-3) / 1e9
         roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                     "traffic": traffic, "peak_source": peaks["_source"] + " hbm_gbs (copy)",
-                    "bytes_per_selection": 4 * M + 12, "frac_of_8TBs": achieved / 8000.0}
+                    "bytes_per_selection": 4 * M + 12, "frac_of_8TBs": achieved / 8000.0,
+                    "row_stats_stream_gbs": rs_gbs}
     else:
         achieved = calls / (ms_step * 1e-3) / 1e9
         mhz = float(peaks.get("sm_max_mhz", 1965.0))

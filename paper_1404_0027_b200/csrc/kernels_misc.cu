@@ -84,9 +84,10 @@ __global__ void __launch_bounds__(kStatsThreads) stats_pass2(const double* part_
     double p = 0.0;
     if (s.valid && mx != 0) p = acc / ((double)M * (double)__uint_as_float(mx));
     s.p = (float)p;
-    // ~8192 expected trials per atomic grab, 32 .. 2048 selections.
+    // ~8192 expected trials per atomic grab, 1 .. 2048 selections (the select kernel raises
+    // it to at least one selection per team of the warp).
     double g = 8192.0 * p;
-    uint32_t grab = g < 32.0 ? 32u : (g > 2048.0 ? 2048u : ((uint32_t)g + 31u) & ~31u);
+    uint32_t grab = g < 1.0 ? 1u : (g > 2048.0 ? 2048u : (uint32_t)g);
     s.grab = grab;
     s.pad = 0;
     *stats = s;

@@ -385,7 +385,7 @@ __global__ void __launch_bounds__(1024, 1) select_shared_kernel(const SharedPara
   const unsigned long long teams = 32u / g;
   const unsigned long long fair = max(1ull, (unsigned long long)K / nwarps);
   const unsigned long long first = max(teams, fair / 2ull);
-  const unsigned long long grab = max(2ull * teams, min((unsigned long long)st.grab, fair / 8ull));
+  const unsigned long long grab = max(teams, min((unsigned long long)st.grab, fair / 8ull));
   Pool pl;
   pool_init(pl, K, nwarps, warp_global, first, grab);
   const TrialStream ts(P.seed_lo, P.seed_hi, P.epoch);

@@ -1,0 +1,10 @@
+#!/bin/bash
+mkdir -p gpurun_out/r12
+timeout 1500 python -m pytest tests -m gpu -x -q > gpurun_out/gpu_tests.log 2>&1
+tail -5 gpurun_out/gpu_tests.log
+for c in c1 c2; do timeout 300 python bench.py --config $c --steps 300 --no-cpu --no-e2e > gpurun_out/r12/$c.json 2>&1; done
+for d in uniform exponential pareto; do for M in 1000 10000 100000; do timeout 300 python bench.py --config c3 --dist $d --M $M --steps 20 --no-cpu --no-e2e > gpurun_out/r12/c3_${d}_$M.json 2>&1; done; done
+timeout 300 python bench.py --config c2 --rule it --steps 300 --no-cpu --no-e2e > gpurun_out/r12/c2_it.json 2>&1
+timeout 600 ncu --set full --clock-control none --import-source on -k regex:"select_shared" -s 3 -c 1 -o gpurun_out/prof_c3e10k_v12 python bench.py --config c3 --dist exponential --M 10000 --steps 2 --warmup 3 --no-cpu --no-e2e > gpurun_out/ncu_c3e10k_v12.log 2>&1
+python scripts/sanitize_cases.py > gpurun_out/r12/san_plain.log 2>&1
+timeout 900 compute-sanitizer --tool memcheck --print-limit 20 python scripts/sanitize_cases.py > gpurun_out/r12/memcheck.log 2>&1; tail -2 gpurun_out/r12/memcheck.log
