@@ -55,8 +55,28 @@ __device__ __forceinline__ bool accept(float t, uint32_t j, uint32_t sbase, cons
 struct Pool {
   unsigned long long next, end;  // current chunk [next, end)
   unsigned long long grab, first;
+  unsigned long long pending;    // lane 0: ticket of the NEXT chunk, fetched one chunk ahead
   uint32_t K, nwarps, stripe;
   bool exhausted;
+
+  // Lane 0 issues the atomic for the chunk after the current one; its latency (~1 us under
+  // contention) overlaps the current chunk's work instead of stalling the warp.
+  __device__ __forceinline__ void prefetch(DevCounters* ctr, uint32_t lane) {
+    if (lane == 0u) pending = dyn_base(stripe) + atomicAdd(&ctr->next[stripe], grab);
+  }
+  // Move to the prefetched chunk (and prefetch the one after); false when the stripe is done.
+  __device__ __forceinline__ bool refill(DevCounters* ctr, uint32_t lane) {
+    const unsigned long long b = __shfl_sync(kFull, pending, 0);
+    const unsigned long long hi = stripe_hi(stripe);
+    if (b >= hi) {
+      exhausted = true;
+      return false;
+    }
+    next = b;
+    end = min(b + grab, hi);
+    prefetch(ctr, lane);
+    return true;
+  }
 
   __device__ __forceinline__ unsigned long long stripe_lo(uint32_t s) const {
     const unsigned long long sz = ((unsigned long long)K + kStripes - 1) / kStripes;
@@ -71,7 +91,7 @@ struct Pool {
 };
 
 __device__ __forceinline__ void pool_init(Pool& pl, uint32_t K, uint32_t nwarps, uint32_t warp_global,
-                                          unsigned long long first, unsigned long long grab) {
+                                          unsigned long long first, unsigned long long grab, DevCounters* ctr) {
   pl.K = K;
   pl.nwarps = nwarps;
   pl.first = first;
@@ -83,6 +103,8 @@ __device__ __forceinline__ void pool_init(Pool& pl, uint32_t K, uint32_t nwarps,
   pl.end = min(lo + first, hi);
   // nothing static and no dynamic part left in the stripe: done without touching the ticket
   pl.exhausted = pl.next >= pl.end && pl.dyn_base(pl.stripe) >= hi;
+  pl.pending = ~0ull;
+  if (pl.dyn_base(pl.stripe) < hi) pl.prefetch(ctr, threadIdx.x & 31u);
 }
 
 // Hand idle teams (leader lanes in `need`) the next selections of the warp's pool.
@@ -91,18 +113,7 @@ __device__ __forceinline__ uint32_t pool_take(Pool& pl, uint32_t need, uint32_t 
                                               DevCounters* ctr) {
   uint32_t got = kNone;
   while (need != 0u && !pl.exhausted) {
-    if (pl.next >= pl.end) {
-      unsigned long long b = 0;
-      if (lane == 0u) b = pl.dyn_base(pl.stripe) + atomicAdd(&ctr->next[pl.stripe], pl.grab);
-      b = __shfl_sync(kFull, b, 0);
-      const unsigned long long hi = pl.stripe_hi(pl.stripe);
-      if (b >= hi) {  // stripe exhausted
-        pl.exhausted = true;
-        break;
-      }
-      pl.next = b;
-      pl.end = min(b + pl.grab, hi);
-    }
+    if (pl.next >= pl.end && !pl.refill(ctr, lane)) break;
     const uint32_t avail = (uint32_t)(pl.end - pl.next);
     const uint32_t r = __popc(need & lanemask_lt());
     uint32_t mine = kNone;
@@ -117,10 +128,10 @@ __device__ __forceinline__ uint32_t pool_take(Pool& pl, uint32_t need, uint32_t 
   return got;
 }
 
-// Trial phase of one warp.  g = lanes per team (power of two); TEAM = (g > 1).
+// Trial phase of one warp with sub-warp teams (1 < g < 32 lanes per selection).
 // Fast path: one Philox call + two gathers + one vote per round; team bookkeeping only
-// when some lane of the warp finished a selection.
-template <int PATH, bool FOLD, bool TEAM>
+// when some team of the warp finished a selection.
+template <int PATH, bool FOLD>
 __device__ __forceinline__ void trial_loop(const SharedParams& P, const TrialStream& ts, uint32_t sbase, float amax,
                                            uint32_t g, Pool pl) {
   const float amax_s = __fmul_rn(amax, 0x1p-24f);
@@ -163,46 +174,28 @@ __device__ __forceinline__ void trial_loop(const SharedParams& P, const TrialStr
       const bool r1 = accept<PATH>(t1, j1, sbase, P.alpha, P.group_shift);
       a0 = active & (c < calls) & r0;
       a1 = active & (c < half) & r1;
-      if constexpr (TEAM) {
-        ball = __ballot_sync(kFull, a0 || a1);
-        out = active && c - rank + g >= calls;   // the team's next round would start past max_trials
-        if (ball != 0u || __any_sync(kFull, out)) break;
-        c += g;
-      } else {
-        out = active && c + 1u >= calls;
-        if (__any_sync(kFull, a0 || a1 || out)) break;
-        ++c;
-      }
+      ball = __ballot_sync(kFull, a0 || a1);
+      out = active && c - rank + g >= calls;   // the team's next round would start past max_trials
+      if (ball != 0u || __any_sync(kFull, out)) break;
+      c += g;
     }
     // slow path: resolve finished selections
-    if constexpr (TEAM) {
-      const uint32_t b = ball & tmask;
-      uint32_t wj = 0, wt = 0;
-      if (ball != 0u) {
-        const uint32_t src = b ? (uint32_t)(__ffs(b) - 1) : lane;
-        wj = __shfl_sync(kFull, a0 ? j0 : j1, src);
-        wt = __shfl_sync(kFull, a0 ? 2u * c + 1u : 2u * c + 2u, src);
-      }
-      if (active) {
-        if (b != 0u || out) {
-          if (leader) {
-            P.idx[my] = b ? (int32_t)wj : -1;
-            if (P.trials) P.trials[my] = b ? wt : P.max_trials;
-          }
-          my = kNone;
-        } else {
-          c += g;
+    const uint32_t b = ball & tmask;
+    uint32_t wj = 0, wt = 0;
+    if (ball != 0u) {
+      const uint32_t src = b ? (uint32_t)(__ffs(b) - 1) : lane;
+      wj = __shfl_sync(kFull, a0 ? j0 : j1, src);
+      wt = __shfl_sync(kFull, a0 ? 2u * c + 1u : 2u * c + 2u, src);
+    }
+    if (active) {
+      if (b != 0u || out) {
+        if (leader) {
+          P.idx[my] = b ? (int32_t)wj : -1;
+          if (P.trials) P.trials[my] = b ? wt : P.max_trials;
         }
-      }
-    } else {
-      if (active) {
-        if (a0 || a1 || out) {
-          P.idx[my] = a0 ? (int32_t)j0 : (a1 ? (int32_t)j1 : -1);
-          if (P.trials) P.trials[my] = a0 ? 2u * c + 1u : (a1 ? 2u * c + 2u : P.max_trials);
-          my = kNone;
-        } else {
-          ++c;
-        }
+        my = kNone;
+      } else {
+        c += g;
       }
     }
   }
@@ -226,18 +219,7 @@ __device__ __forceinline__ void lane_loop(const SharedParams& P, const TrialStre
   while (true) {
     if (need != 0u) {  // warp-uniform: hand out selections
       while (need != 0u && !pl.exhausted) {
-        if (pl.next >= pl.end) {
-          unsigned long long b = 0;
-          if (lane == 0u) b = pl.dyn_base(pl.stripe) + atomicAdd(&P.ctr->next[pl.stripe], pl.grab);
-          b = __shfl_sync(kFull, b, 0);
-          const unsigned long long hi = pl.stripe_hi(pl.stripe);
-          if (b >= hi) {
-            pl.exhausted = true;
-            break;
-          }
-          pl.next = b;
-          pl.end = min(b + pl.grab, hi);
-        }
+        if (pl.next >= pl.end && !pl.refill(P.ctr, lane)) break;
         const uint32_t avail = (uint32_t)(pl.end - pl.next);
         const uint32_t r = __popc(need & lt);
         const bool mine = ((need >> lane) & 1u) && r < avail;
@@ -282,15 +264,7 @@ __device__ __forceinline__ void warp_loop(const SharedParams& P, const TrialStre
   const uint32_t calls = half + (P.max_trials & 1u);
   const uint32_t lane = threadIdx.x & 31u;
   while (!pl.exhausted) {
-    if (pl.next >= pl.end) {
-      unsigned long long b = 0;
-      if (lane == 0u) b = pl.dyn_base(pl.stripe) + atomicAdd(&P.ctr->next[pl.stripe], pl.grab);
-      b = __shfl_sync(kFull, b, 0);
-      const unsigned long long hi = pl.stripe_hi(pl.stripe);
-      if (b >= hi) break;
-      pl.next = b;
-      pl.end = min(b + pl.grab, hi);
-    }
+    if (pl.next >= pl.end && !pl.refill(P.ctr, lane)) break;
     const uint32_t my = (uint32_t)pl.next++;
     const uint32_t sel = ts.sel_word(P.s0 + my);
     int32_t id = -1;
@@ -387,7 +361,7 @@ __global__ void __launch_bounds__(1024, 1) select_shared_kernel(const SharedPara
   const unsigned long long first = max(teams, fair / 2ull);
   const unsigned long long grab = max(teams, min((unsigned long long)st.grab, fair / 8ull));
   Pool pl;
-  pool_init(pl, K, nwarps, warp_global, first, grab);
+  pool_init(pl, K, nwarps, warp_global, first, grab, P.ctr);
   const TrialStream ts(P.seed_lo, P.seed_hi, P.epoch);
   const bool fold = can_fold(st.amax_bits);
   if (g == 1u) {
@@ -402,9 +376,9 @@ __global__ void __launch_bounds__(1024, 1) select_shared_kernel(const SharedPara
       warp_loop<PATH, false>(P, ts, sbase, amax, pl);
   } else {
     if (fold)
-      trial_loop<PATH, true, true>(P, ts, sbase, amax, g, pl);
+      trial_loop<PATH, true>(P, ts, sbase, amax, g, pl);
     else
-      trial_loop<PATH, false, true>(P, ts, sbase, amax, g, pl);
+      trial_loop<PATH, false>(P, ts, sbase, amax, g, pl);
   }
 
   // ---- the last CTA out resets the work-stealing ticket for the next launch
