@@ -193,6 +193,8 @@ int launch_select(gpuar_handle* h, const float* alpha, int64_t rows, int64_t ld,
     p.group_shift = h->group_shift;
     p.smem_bytes = h->shared_smem;
     p.w = h->w;
+    p.grab_override = (uint32_t)std::max(0, env_int("GPUAR_GRAB", 0));
+    p.no_prefetch = (uint32_t)env_int("GPUAR_NO_PREFETCH", 0);
     if (h->rule == kRuleArgmin) {
       e = launch_argmin_shared(p, h->am_smem, h->am_grid, 256, st);
     } else if (h->rule == kRuleIT) {

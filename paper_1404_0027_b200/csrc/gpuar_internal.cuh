@@ -61,6 +61,8 @@ struct SharedParams {
   uint32_t group_shift;      // path 3: log2(group size)
   uint32_t smem_bytes;       // bytes of the staged vector / prefilter
   float w;                   // argmin rule: T = fl32(w * alpha_max)
+  uint32_t grab_override;    // tuning: fixed selections per ticket grab (0 = model)
+  uint32_t no_prefetch;      // tuning: 1 = fetch tickets on demand
 };
 
 struct RowsParams {

@@ -61,11 +61,13 @@ struct Pool {
 
   // Lane 0 issues the atomic for the chunk after the current one; its latency (~1 us under
   // contention) overlaps the current chunk's work instead of stalling the warp.
+  bool ahead;                    // prefetch one chunk ahead (else fetch on demand)
   __device__ __forceinline__ void prefetch(DevCounters* ctr, uint32_t lane) {
     if (lane == 0u) pending = dyn_base(stripe) + atomicAdd(&ctr->next[stripe], grab);
   }
   // Move to the prefetched chunk (and prefetch the one after); false when the stripe is done.
   __device__ __forceinline__ bool refill(DevCounters* ctr, uint32_t lane) {
+    if (!ahead) prefetch(ctr, lane);
     const unsigned long long b = __shfl_sync(kFull, pending, 0);
     const unsigned long long hi = stripe_hi(stripe);
     if (b >= hi) {
@@ -74,7 +76,7 @@ struct Pool {
     }
     next = b;
     end = min(b + grab, hi);
-    prefetch(ctr, lane);
+    if (ahead) prefetch(ctr, lane);
     return true;
   }
 
@@ -91,7 +93,9 @@ struct Pool {
 };
 
 __device__ __forceinline__ void pool_init(Pool& pl, uint32_t K, uint32_t nwarps, uint32_t warp_global,
-                                          unsigned long long first, unsigned long long grab, DevCounters* ctr) {
+                                          unsigned long long first, unsigned long long grab, DevCounters* ctr,
+                                          bool ahead) {
+  pl.ahead = ahead;
   pl.K = K;
   pl.nwarps = nwarps;
   pl.first = first;
@@ -104,7 +108,7 @@ __device__ __forceinline__ void pool_init(Pool& pl, uint32_t K, uint32_t nwarps,
   // nothing static and no dynamic part left in the stripe: done without touching the ticket
   pl.exhausted = pl.next >= pl.end && pl.dyn_base(pl.stripe) >= hi;
   pl.pending = ~0ull;
-  if (pl.dyn_base(pl.stripe) < hi) pl.prefetch(ctr, threadIdx.x & 31u);
+  if (ahead && pl.dyn_base(pl.stripe) < hi) pl.prefetch(ctr, threadIdx.x & 31u);
 }
 
 // Hand idle teams (leader lanes in `need`) the next selections of the warp's pool.
@@ -355,13 +359,16 @@ __global__ void __launch_bounds__(1024, 1) select_shared_kernel(const SharedPara
   __syncthreads();
   const uint32_t g = s_g;
   // static first chunk: half of a warp's fair share; then grabs of ~8192 expected trials
-  // (st.grab), at most an eighth of the fair share, at least one selection per team.
+  // (st.grab), at most an eighth of the fair share (but two teams' worth), at least one
+  // selection per team; tickets are prefetched one chunk ahead.
   const unsigned long long teams = 32u / g;
   const unsigned long long fair = max(1ull, (unsigned long long)K / nwarps);
   const unsigned long long first = max(teams, fair / 2ull);
-  const unsigned long long grab = max(teams, min((unsigned long long)st.grab, fair / 8ull));
+  // (r01 sweep, GPUAR_GRAB: c2 best at 2 with prefetch; heavy tails (st.grab = 1) at 1)
+  unsigned long long grab = max(teams, min((unsigned long long)st.grab, max(2ull * teams, fair / 8ull)));
+  if (P.grab_override) grab = P.grab_override;
   Pool pl;
-  pool_init(pl, K, nwarps, warp_global, first, grab, P.ctr);
+  pool_init(pl, K, nwarps, warp_global, first, grab, P.ctr, P.no_prefetch == 0u);
   const TrialStream ts(P.seed_lo, P.seed_hi, P.epoch);
   const bool fold = can_fold(st.amax_bits);
   if (g == 1u) {
