@@ -29,8 +29,8 @@ namespace {
 // Trials of one row by one warp: round t = Philox calls [32t, 32t+32), lane l -> call
 // 32t + l -> trials 2c, 2c+1; the ballot's lowest lane (even trial first) is the first
 // accept in canonical order (R6).
-template <bool FOLD>
-__device__ __forceinline__ void row_trials(const TrialStream& ts, uint32_t sel, uint32_t row_s, uint32_t M,
+template <bool FOLD, class Stream>
+__device__ __forceinline__ void row_trials(const Stream& ts, uint32_t sel, uint32_t row_s, uint32_t M,
                                            float amax, uint32_t half, uint32_t calls, uint32_t lane, int32_t& id,
                                            uint32_t& tr) {
   const float amax_s = __fmul_rn(amax, 0x1p-24f);
@@ -55,8 +55,8 @@ __device__ __forceinline__ void row_trials(const TrialStream& ts, uint32_t sel, 
 
 // The paper's printed rule on one row (R16-R19): lane l rates reactions 4c..4c+3
 // of its calls c = l, l+32, ...; warp butterfly on the (rating bits, index) key.
-template <bool FOLD>
-__device__ __forceinline__ void row_argmin(const TrialStream& ts, uint32_t sel, uint32_t row_s, uint32_t M, float T,
+template <bool FOLD, class Stream>
+__device__ __forceinline__ void row_argmin(const Stream& ts, uint32_t sel, uint32_t row_s, uint32_t M, float T,
                                            uint32_t lane, int32_t& id) {
   const float T_s = __fmul_rn(T, 0x1p-24f);
   const uint32_t k1t = ts.rk1[0] ^ kTagElection;
