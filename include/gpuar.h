@@ -125,7 +125,7 @@ int gpuar_select_host(gpuar_t h, const float *h_alpha, int64_t rows, int64_t ld,
  *     counter {0, s_g, epoch, 2}; idx = the smallest j with C_j > u2 * alpha_0, C_j the
  *     sequential binary64 prefix sum (computed once per registered vector, O(M)); trials = 1.
  * Applies to later gpuar_select / gpuar_select_host calls (shared vector and matrix; IT:
- * gpuar_select on a matrix returns EINVAL).
+ * gpuar_select / gpuar_select_host on a matrix return EINVAL).
  * Errors: EINVAL (unknown rule, w out of range). */
 #define GPUAR_RULE_CLASSIC 0
 #define GPUAR_RULE_ARGMIN  1

@@ -391,6 +391,7 @@ int gpuar_select_host(gpuar_t h, const float* h_alpha, int64_t rows, int64_t ld,
   if (!h || !h_alpha || !h_idx || !h_tau || !h_trials || K < 1 || K > h->Kcap) return GPUAR_EINVAL;
   if (!(rows == 1 || rows == K)) return GPUAR_EINVAL;
   if (rows != 1 && ld < h->M) return GPUAR_EINVAL;
+  if (rows != 1 && h->rule == kRuleIT) return GPUAR_EINVAL;  // IT: shared vector only
   if (h->offset + (uint64_t)K > (1ull << 32)) return GPUAR_EINVAL;
   DeviceGuard g(h->device);
   if (!g.ok) return GPUAR_ECUDA;

@@ -430,6 +430,8 @@ def test_it_law_and_rows_refused():
     sel2.set_propensities(torch.ones((8, 4), device="cuda"))
     with pytest.raises(GpuarError):
         sel2.select(8)
+    with pytest.raises(GpuarError):
+        sel2.select_host(torch.ones((8, 4)))
 
 
 # ---------------------------------------------------------------- full-size shared-vector configs
@@ -484,3 +486,40 @@ def test_c5_full_size_sampled():
     assert (gi >= 0).all() and (a[gi] > 0).all()
     p = oracle.acceptance_rate(a)
     assert abs(gtr.astype(np.float64).mean() - 1 / p) < 5 * math.sqrt((1 - p) / K) / p
+
+
+# ---------------------------------------------------------------- argument checking through the ABI
+
+def test_abi_error_paths():
+    from paper_1404_0027_b200 import GpuarError, Selector
+    sel = Selector(8, 16, SEED)
+    with pytest.raises(GpuarError) as e:
+        sel.select(16)                                    # nothing registered
+    assert e.value.status == -4
+    with pytest.raises(GpuarError) as e:
+        sel.stats()
+    assert e.value.status == -4
+    base = torch.zeros(16 * 8 + 4, device="cuda")
+    with pytest.raises(GpuarError) as e:                  # matrix base not 16-byte aligned
+        sel.set_propensities(base[1:1 + 16 * 8].view(16, 8))
+    assert e.value.status == -1
+    sel.set_propensities(torch.ones(8, device="cuda"))
+    with pytest.raises(GpuarError):
+        sel.select(17)                                    # K > capacity
+    sel.set_selection_offset((1 << 32) - 8)
+    with pytest.raises(GpuarError):
+        sel.select(16)                                    # offset + K > 2^32
+    with pytest.raises(GpuarError):
+        sel.set_selection_offset(1 << 32)
+    with pytest.raises(GpuarError):
+        sel.set_max_trials(0)
+    sel.set_selection_offset(0)
+    idx, _, _ = sel.select(16)
+    sel.sync()
+    assert (idx.cpu() >= 0).all()
+    m = Selector(8, 4, SEED)
+    m.set_propensities(torch.ones((4, 8), device="cuda"))
+    with pytest.raises(GpuarError):
+        m.select(3)                                       # K != rows for a matrix
+    with pytest.raises(GpuarError):
+        m.stats()                                         # stats are for shared vectors
