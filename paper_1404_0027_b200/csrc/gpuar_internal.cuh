@@ -22,7 +22,7 @@ struct DevStats {
 };
 
 // Per-handle device counters.
-constexpr uint32_t kStripes = 16;  // work-stealing tickets, one per stripe of selections
+constexpr uint32_t kStripes = 64;  // work-stealing tickets, one per stripe of selections
 struct DevCounters {
   unsigned long long next[kStripes];  // tickets (reset by the last CTA of each launch)
   unsigned int done;                  // CTAs finished in the current launch
