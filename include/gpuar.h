@@ -74,7 +74,9 @@ int gpuar_create(gpuar_t *out, int64_t M, int64_t K, uint64_t seed);
 int gpuar_destroy(gpuar_t h);
 
 /* Enqueue all later work on `stream` (a cudaStream_t of the handle's device, passed as
- * void* so this header does not need the CUDA headers). */
+ * void* so this header does not need the CUDA headers).  The new stream is ordered after
+ * the work already queued on the previous one (event wait): a handle's launches share its
+ * device scratch and must never overlap.  Use one handle per concurrent stream. */
 int gpuar_set_stream(gpuar_t h, void *stream);
 
 /* Register the propensities (device pointer, binary32, BORROWED).

@@ -87,6 +87,7 @@ struct gpuar_handle {
   bool prefix_valid = false;
   uint32_t ssa_net_bytes = 0, ssa_warp_bytes = 0;
   Chunked host;
+  cudaEvent_t order_ev = nullptr;  // orders a new stream after the old one (gpuar_set_stream)
 };
 
 namespace {
@@ -345,13 +346,27 @@ int gpuar_destroy(gpuar_t h) {
   cudaFree(h->d_part_max);
   cudaFree(h->d_pref);
   cudaFree(h->d_prefix);
+  if (h->order_ev) cudaEventDestroy(h->order_ev);
   delete h;
   return e == cudaSuccess ? GPUAR_OK : GPUAR_ECUDA;
 }
 
 int gpuar_set_stream(gpuar_t h, void* stream) {
   if (!h) return GPUAR_EINVAL;
-  h->stream = static_cast<cudaStream_t>(stream);
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  if (s == h->stream) return GPUAR_OK;
+  // The handle's device scratch (work-stealing tickets, statistics) is shared by all its
+  // launches: order the new stream after everything already queued on the old one.
+  DeviceGuard g(h->device);
+  if (!g.ok) return GPUAR_ECUDA;
+  if (!h->order_ev) {
+    cudaError_t e = cudaEventCreateWithFlags(&h->order_ev, cudaEventDisableTiming);
+    if (e != cudaSuccess) return cuda_status(e);
+  }
+  cudaError_t e = cudaEventRecord(h->order_ev, h->stream);
+  if (e == cudaSuccess) e = cudaStreamWaitEvent(s, h->order_ev, 0);
+  if (e != cudaSuccess) return cuda_status(e);
+  h->stream = s;
   return GPUAR_OK;
 }
 

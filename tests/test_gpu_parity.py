@@ -523,3 +523,20 @@ def test_abi_error_paths():
         m.select(3)                                       # K != rows for a matrix
     with pytest.raises(GpuarError):
         m.stats()                                         # stats are for shared vectors
+
+
+def test_stream_switch_keeps_handle_work_ordered():
+    """Back-to-back selections issued on two different torch streams through one handle must
+    not overlap (they share the work-stealing tickets): results equal the oracle's."""
+    a = synth.exponential(1000)
+    K = 200_000
+    sel = _sel(a.size, K)
+    s1, s2 = torch.cuda.Stream(), torch.cuda.Stream()
+    with torch.cuda.stream(s1):
+        sel.set_propensities(torch.from_numpy(a).cuda())
+        o1 = sel.select(K)
+    with torch.cuda.stream(s2):
+        o2 = sel.select(K)
+    torch.cuda.synchronize()
+    np.testing.assert_array_equal(o1[0].cpu().numpy(), oracle.ar_select(a, K, seed=SEED, epoch=0, nthreads=8)["idx"])
+    np.testing.assert_array_equal(o2[0].cpu().numpy(), oracle.ar_select(a, K, seed=SEED, epoch=1, nthreads=8)["idx"])
