@@ -141,7 +141,10 @@ int gpuar_set_rule(gpuar_t h, int rule, float w);
  * change vector v_j (species -1 = unused slot; species distinct within a reaction).
  * Propensity a_j = c_j, c_j X_a, c_j X_a X_b, or c_j X_a (X_a - 1) / 2 (+0 if X_a < 2), in
  * binary32 left to right (R20).  The network plus one realization's state and
- * row (4M + 4N bytes) must fit in shared memory (EINVAL otherwise).
+ * row (4M + 4N bytes) must fit in shared memory (EINVAL otherwise).  gpuar_set_network is
+ * SYNCHRONOUS: it reads the network once to build, per reaction j, the list of reactions
+ * whose propensity reads a species j changes (only those are recomputed after j fires;
+ * the row stays identical to a full recomputation); EINVAL for species indices >= N.
  * gpuar_ssa_run advances K realizations (d_X[K][N] int32 and d_t[K] binary64, in place)
  * by up to n_steps steps each: step i of realization k (selection s_g = offset + k) uses
  * epoch + i: propensities, classic-AR selection and tau exactly as gpuar_select on that

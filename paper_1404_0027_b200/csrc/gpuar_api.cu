@@ -7,6 +7,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <new>
+#include <vector>
 
 #include "../../include/gpuar.h"
 #include "gpuar_internal.cuh"
@@ -82,6 +83,10 @@ struct gpuar_handle {
   const int32_t* net_dval = nullptr;
   int64_t net_N = 0, net_D = 0;
   int ssa_warps = 0, ssa_grid = 0;
+  int32_t* d_dep_ptr = nullptr;  // dependency lists of the registered network (handle-owned)
+  int32_t* d_dep_idx = nullptr;
+  uint32_t dep_total = 0;
+  bool ssa_deps = false;
   // inverse transform (GPUAR_RULE_IT): sequential binary64 prefix sums of the shared vector
   double* d_prefix = nullptr;
   bool prefix_valid = false;
@@ -347,6 +352,8 @@ int gpuar_destroy(gpuar_t h) {
   cudaFree(h->d_pref);
   cudaFree(h->d_prefix);
   if (h->order_ev) cudaEventDestroy(h->order_ev);
+  cudaFree(h->d_dep_ptr);
+  cudaFree(h->d_dep_idx);
   delete h;
   return e == cudaSuccess ? GPUAR_OK : GPUAR_ECUDA;
 }
@@ -525,14 +532,65 @@ int gpuar_set_network(gpuar_t h, int64_t N, int64_t D, const int32_t* d_reac, co
   if (!h || !d_reac || !d_rate || !d_didx || !d_dval || N < 1 || N > 0x7fffffffll || D < 1 || D > 32)
     return GPUAR_EINVAL;
   const uint64_t M = (uint64_t)h->M;
-  const uint64_t net = ((M * (16u + 8u * (uint64_t)D)) + 15u) & ~15ull;  // int4 descriptors + didx/dval
-  const uint64_t per_warp = ((4u * M + 15u) & ~15ull) + ((4u * ((uint64_t)N + 1u) + 15u) & ~15ull);
-  const uint64_t budget = (uint64_t)h->smem_optin - 1024u;
-  if (net + per_warp > budget) return GPUAR_EINVAL;  // network + one realization must fit on chip
-  int W = (int)std::min<uint64_t>(24, (budget - net) / per_warp);
-  const size_t sh = (size_t)net + (size_t)W * per_warp;
   DeviceGuard g(h->device);
   if (!g.ok) return GPUAR_ECUDA;
+  // Dependency lists (host, once per network): reaction j changes species S_j; the
+  // propensities to refresh after j fires are the reactions with a reactant in S_j.
+  std::vector<int32_t> reac(2 * M), didx(M * D), dval(M * D);
+  cudaError_t e = cudaMemcpy(reac.data(), d_reac, 8 * M, cudaMemcpyDeviceToHost);
+  if (e == cudaSuccess) e = cudaMemcpy(didx.data(), d_didx, 4 * M * D, cudaMemcpyDeviceToHost);
+  if (e == cudaSuccess) e = cudaMemcpy(dval.data(), d_dval, 4 * M * D, cudaMemcpyDeviceToHost);
+  if (e != cudaSuccess) return cuda_status(e);
+  std::vector<std::vector<int32_t>> users((size_t)N);
+  for (uint64_t j = 0; j < M; ++j) {
+    const int32_t r0 = reac[2 * j], r1 = reac[2 * j + 1];
+    if (r0 >= N || r1 >= N) return GPUAR_EINVAL;
+    if (r0 >= 0) users[r0].push_back((int32_t)j);
+    if (r1 >= 0 && r1 != r0) users[r1].push_back((int32_t)j);
+  }
+  std::vector<int32_t> ptr(M + 1, 0), idx;
+  std::vector<char> mark(M, 0);
+  for (uint64_t j = 0; j < M; ++j) {
+    std::vector<int32_t> dep;
+    for (int64_t d = 0; d < D; ++d) {
+      const int32_t sp = didx[j * D + d];
+      if (sp >= N) return GPUAR_EINVAL;
+      if (sp < 0 || dval[j * D + d] == 0) continue;
+      for (int32_t r : users[sp])
+        if (!mark[r]) {
+          mark[r] = 1;
+          dep.push_back(r);
+        }
+    }
+    std::sort(dep.begin(), dep.end());
+    for (int32_t r : dep) mark[r] = 0;
+    idx.insert(idx.end(), dep.begin(), dep.end());
+    ptr[j + 1] = (int32_t)idx.size();
+  }
+  const uint64_t net0 = ((M * (16u + 8u * (uint64_t)D)) + 15u) & ~15ull;  // int4 descriptors + didx/dval
+  const uint64_t dep_bytes = ((4u * (M + 1u + idx.size())) + 15u) & ~15ull;
+  const uint64_t per_warp = ((4u * M + 15u) & ~15ull) + ((4u * ((uint64_t)N + 1u) + 15u) & ~15ull);
+  const uint64_t budget = (uint64_t)h->smem_optin - 1024u;
+  if (net0 + per_warp > budget) return GPUAR_EINVAL;  // network + one realization must fit on chip
+  // keep the dependency lists on chip if at least 8 warps still fit, else recompute every step
+  const bool deps = net0 + dep_bytes + 8u * per_warp <= budget;
+  const uint64_t net = net0 + (deps ? dep_bytes : 0u);
+  int W = (int)std::min<uint64_t>(24, (budget - net) / per_warp);
+  const size_t sh = (size_t)net + (size_t)W * per_warp;
+  cudaFree(h->d_dep_ptr);
+  cudaFree(h->d_dep_idx);
+  h->d_dep_ptr = h->d_dep_idx = nullptr;
+  h->dep_total = 0;
+  if (deps) {
+    e = cudaMalloc(&h->d_dep_ptr, 4 * (M + 1));
+    if (e == cudaSuccess) e = cudaMalloc(&h->d_dep_idx, 4 * std::max<size_t>(1, idx.size()));
+    if (e == cudaSuccess) e = cudaMemcpy(h->d_dep_ptr, ptr.data(), 4 * (M + 1), cudaMemcpyHostToDevice);
+    if (e == cudaSuccess && !idx.empty())
+      e = cudaMemcpy(h->d_dep_idx, idx.data(), 4 * idx.size(), cudaMemcpyHostToDevice);
+    if (e != cudaSuccess) return cuda_status(e);
+    h->dep_total = (uint32_t)idx.size();
+  }
+  h->ssa_deps = deps;
   const int n = ssa_blocks_per_sm(W, sh);
   if (n <= 0) return GPUAR_EINVAL;
   h->net_reac = d_reac;
@@ -576,6 +634,9 @@ int gpuar_ssa_run(gpuar_t h, int32_t* d_X, double* d_t, uint32_t* d_steps, int64
   p.n_steps = n_steps;
   p.net_bytes = h->ssa_net_bytes;
   p.warp_bytes = h->ssa_warp_bytes;
+  p.dep_ptr = h->ssa_deps ? h->d_dep_ptr : nullptr;
+  p.dep_idx = h->ssa_deps ? h->d_dep_idx : nullptr;
+  p.dep_total = h->dep_total;
   const int grid = (int)std::min<int64_t>(h->ssa_grid, (K + h->ssa_warps - 1) / h->ssa_warps);
   const int st = cuda_status(launch_ssa(p, std::max(grid, 1), h->ssa_warps, h->stream));
   if (st == GPUAR_OK) h->epoch += (uint32_t)n_steps;

@@ -101,8 +101,11 @@ struct SsaParams {
   uint32_t N, M, D, K;
   uint32_t s0, epoch0, seed_lo, seed_hi, max_trials;
   int32_t n_steps;
-  uint32_t net_bytes;    // staged network (smem)
+  uint32_t net_bytes;    // staged network (smem), including the dependency lists
   uint32_t warp_bytes;   // per-warp row + state (smem)
+  const int32_t* dep_ptr;  // M+1 CSR offsets: reactions whose propensity reads a species
+  const int32_t* dep_idx;  // that reaction j changes (null: recompute every propensity)
+  uint32_t dep_total;
 };
 
 // ---------------------------------------------------------------- PTX helpers

@@ -74,6 +74,14 @@ __global__ void __launch_bounds__(768, 1) ssa_kernel(const SsaParams P) {
     s_didx[i] = P.didx[i];
     s_dval[i] = P.dval[i];
   }
+  // dependency lists (CSR): after reaction j fires only its dependents' propensities change
+  int32_t* s_dptr = s_dval + D * M;
+  int32_t* s_didxs = s_dptr + (M + 1u);
+  const bool deps = P.dep_ptr != nullptr;
+  if (deps) {
+    for (uint32_t i = threadIdx.x; i <= M; i += blockDim.x) s_dptr[i] = P.dep_ptr[i];
+    for (uint32_t i = threadIdx.x; i < P.dep_total; i += blockDim.x) s_didxs[i] = P.dep_idx[i];
+  }
   __syncthreads();
   const uint32_t desc_s = smem_u32(s_desc);
   unsigned char* mine = smem + P.net_bytes + (size_t)warp * P.warp_bytes;
@@ -96,8 +104,13 @@ __global__ void __launch_bounds__(768, 1) ssa_kernel(const SsaParams P) {
     uint32_t fired = 0;
     const uint32_t s = P.s0 + k;
     __syncwarp();
+    float nlog = 0.f;  // -ln(u1) of step (step & ~31) + lane: tau draws 32 steps at a time
     for (int32_t step = 0; step < P.n_steps; ++step) {
-      // ---- propensities -> row, with alpha_max (bits) and alpha_0 as in kernels_rows.cu
+      if ((step & 31) == 0) nlog = neg_log_u1(P.seed_lo, P.seed_hi, s, P.epoch0 + (uint32_t)(step + (int32_t)lane));
+      // ---- propensities -> row (all of them on the first step of the call, else only the
+      // dependents of the last fired reaction, already updated below), with alpha_max (bits)
+      // and alpha_0 reduced over the whole row in a fixed order (as in kernels_rows.cu)
+      const bool full = step == 0 || !deps;
       uint32_t mx = 0;
       double acc = 0.0;
       for (uint32_t ch = 0; ch < full_chunks; ++ch) {
@@ -105,8 +118,12 @@ __global__ void __launch_bounds__(768, 1) ssa_kernel(const SsaParams P) {
 #pragma unroll
         for (int q = 0; q < 8; ++q) {
           const uint32_t j = ch * 256u + (uint32_t)q * 32u + lane;
-          v[q] = propensity(xs, lds_i4(desc_s + 16u * j));
-          row[j] = v[q];
+          if (full) {
+            v[q] = propensity(xs, lds_i4(desc_s + 16u * j));
+            row[j] = v[q];
+          } else {
+            v[q] = lds_f32(row_s + 4u * j);
+          }
           mx = max(mx, __float_as_uint(v[q]));
         }
         acc += (double)__fadd_rn(__fadd_rn(__fadd_rn(v[0], v[1]), __fadd_rn(v[2], v[3])),
@@ -115,8 +132,13 @@ __global__ void __launch_bounds__(768, 1) ssa_kernel(const SsaParams P) {
       {
         float sum = 0.f;
         for (uint32_t j = (full_chunks << 8) + lane; j < M; j += 32u) {
-          const float v = propensity(xs, lds_i4(desc_s + 16u * j));
-          row[j] = v;
+          float v;
+          if (full) {
+            v = propensity(xs, lds_i4(desc_s + 16u * j));
+            row[j] = v;
+          } else {
+            v = lds_f32(row_s + 4u * j);
+          }
           mx = max(mx, __float_as_uint(v));
           sum = __fadd_rn(sum, v);
         }
@@ -132,7 +154,7 @@ __global__ void __launch_bounds__(768, 1) ssa_kernel(const SsaParams P) {
       }
       if (mx == 0u) break;  // nothing can fire: halted
       const uint32_t epoch = P.epoch0 + (uint32_t)step;
-      const float tau = __fdiv_rn(neg_log_u1(P.seed_lo, P.seed_hi, s, epoch), __double2float_rn(acc));
+      const float tau = __fdiv_rn(__shfl_sync(kFull, nlog, step & 31), __double2float_rn(acc));
       if (t + (double)tau > P.t_end) break;  // the next event is past t_end
       ts.set_epoch(epoch);
       int32_t id = -1;
@@ -148,6 +170,14 @@ __global__ void __launch_bounds__(768, 1) ssa_kernel(const SsaParams P) {
         }
         t += (double)tau;
         ++fired;
+        if (deps) {  // refresh the propensities that read a changed species
+          __syncwarp();
+          const int32_t d0 = s_dptr[id], d1 = s_dptr[id + 1];
+          for (int32_t d = d0 + (int32_t)lane; d < d1; d += 32) {
+            const uint32_t j = (uint32_t)s_didxs[d];
+            row[j] = propensity(xs, lds_i4(desc_s + 16u * j));
+          }
+        }
       }
       __syncwarp();
     }
