@@ -4,15 +4,16 @@
 //
 // Design (B200-first, not the paper's election/argmin kernels of PAPER.md:498-555):
 //  * one persistent launch; the vector (or an exact prefilter of it) is staged once per
-//    CTA in shared memory;
-//  * a selection is worked by a TEAM of g lanes (g = 1..32, a power of two picked on the
-//    device from K and p): in round q lane `rank` makes Philox call c = q*g + rank, i.e.
-//    trials 2c and 2c+1, so a round covers the contiguous trial block [2qg, 2(q+1)g).
-//    The team's ballot + __ffs picks the lowest accepting lane, and within it the even
-//    trial first -> the globally smallest accepted trial index, independent of g;
-//  * teams that finish take the next selection from a warp-local pool refilled by one
-//    64-bit atomic per `grab` selections (work stealing: no tail from geometric trial
-//    counts);
+//    CTA in shared memory by one bulk async copy;
+//  * a selection is worked by a TEAM of g lanes (g = 1..32, a power of two picked once per
+//    CTA from K and p by an instruction-count model): in round q lane `rank` makes Philox
+//    call c = q*g + rank, i.e. trials 2c and 2c+1, so a round covers the contiguous trial
+//    block [2qg, 2(q+1)g).  The team's ballot + __ffs picks the lowest accepting lane, and
+//    within it the even trial first -> the globally smallest accepted trial index,
+//    independent of g.  g = 32 runs warp_loop, g = 1 lane_loop, others trial_loop;
+//  * teams that finish take the next selection from a warp-local pool refilled from one of
+//    64 striped tickets (one 64-bit atomic per `grab` selections, prefetched one chunk
+//    ahead): work stealing, so geometric trial counts leave no long tail;
 //  * tau is a separate, fully coalesced grid-stride phase.
 #include <algorithm>
 
@@ -50,8 +51,8 @@ __device__ __forceinline__ bool accept(float t, uint32_t j, uint32_t sbase, cons
 // belongs to stripe w % kStripes, takes a static first chunk of it, then grabs `grab`
 // selections at a time from the stripe's ticket until the stripe is exhausted.  kStripes
 // tickets keep same-address atomic contention low; a warp never leaves its stripe (a
-// stripe holds K/16 selections, so stripes finish within ~1/sqrt(K/16) of each other),
-// so each warp makes at most one failing atomic.
+// stripe holds K/kStripes selections, so stripes finish within ~1/sqrt(K/kStripes) of
+// each other), so each warp makes at most one failing atomic.
 struct Pool {
   unsigned long long next, end;  // current chunk [next, end)
   unsigned long long grab, first;
