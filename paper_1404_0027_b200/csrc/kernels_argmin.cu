@@ -23,10 +23,14 @@ namespace gpuar {
 
 namespace {
 
-__device__ __forceinline__ unsigned long long rating_key(float t, float d, uint32_t j) {
-  // election: eligible iff t < d (d = 0 is never eligible since t >= 0); rating t / d
+// election: eligible iff t < d (d = 0 is never eligible since t >= 0), rating t / d; a
+// lane sees its reactions in increasing j, so a strict `<` keeps the lowest index on ties.
+__device__ __forceinline__ void elect(float t, float d, uint32_t j, float& bestR, uint32_t& bestJ) {
   const float R = (t < d) ? __fdiv_rn(t, d) : 1.0f;
-  return ((unsigned long long)__float_as_uint(R) << 32) | j;
+  if (R < bestR) {
+    bestR = R;
+    bestJ = j;
+  }
 }
 
 template <bool SMEM, bool FOLD>
@@ -39,7 +43,6 @@ __device__ __forceinline__ void argmin_teams(const SharedParams& P, uint32_t sba
   const uint32_t tid = blockIdx.x * blockDim.x + threadIdx.x;
   const uint32_t nteams = (gridDim.x * blockDim.x) / g;
   const TrialStream ts(P.seed_lo, P.seed_hi, P.epoch, kTagElection);
-  const unsigned long long none = ((unsigned long long)0x3f800000u << 32) | 0xffffffffull;
   // every lane of a warp runs the same number of iterations (K rounded up per warp)
   const uint32_t team0 = tid / g;
   const uint32_t warp_teams = 32u / g;
@@ -49,7 +52,8 @@ __device__ __forceinline__ void argmin_teams(const SharedParams& P, uint32_t sba
     const uint32_t s = base + team_in_warp;
     const bool live = s < K;
     const uint32_t sel = ts.sel_word(P.s0 + s);
-    unsigned long long best = none;
+    float bestR = 1.0f;  // sentinel: nothing eligible yet
+    uint32_t bestJ = 0xffffffffu;
     for (uint32_t c = rank; c < calls; c += g) {
       const Philox4 x = ts(c, sel);
       const uint32_t j = 4u * c;
@@ -62,11 +66,13 @@ __device__ __forceinline__ void argmin_teams(const SharedParams& P, uint32_t sba
         d.z = j + 2u < M ? __ldg(P.alpha + j + 2u) : 0.f;
         d.w = j + 3u < M ? __ldg(P.alpha + j + 3u) : 0.f;
       }
-      best = min(best, rating_key(scaled_u<FOLD>(x.x, T, T_s), d.x, j));
-      best = min(best, rating_key(scaled_u<FOLD>(x.y, T, T_s), d.y, j + 1u));
-      best = min(best, rating_key(scaled_u<FOLD>(x.z, T, T_s), d.z, j + 2u));
-      best = min(best, rating_key(scaled_u<FOLD>(x.w, T, T_s), d.w, j + 3u));
+      elect(scaled_u<FOLD>(x.x, T, T_s), d.x, j, bestR, bestJ);
+      elect(scaled_u<FOLD>(x.y, T, T_s), d.y, j + 1u, bestR, bestJ);
+      elect(scaled_u<FOLD>(x.z, T, T_s), d.z, j + 2u, bestR, bestJ);
+      elect(scaled_u<FOLD>(x.w, T, T_s), d.w, j + 3u, bestR, bestJ);
     }
+    // team minimum of the lexicographic (rating bits, index) key
+    unsigned long long best = ((unsigned long long)__float_as_uint(bestR) << 32) | bestJ;
     for (uint32_t o = g >> 1; o > 0; o >>= 1) best = min(best, __shfl_xor_sync(kFull, best, o));
     if (live && rank == 0u) {
       const bool ok = (uint32_t)(best >> 32) < 0x3f800000u;  // some rating < 1

@@ -61,7 +61,8 @@ __device__ __forceinline__ void row_argmin(const Stream& ts, uint32_t sel, uint3
   const float T_s = __fmul_rn(T, 0x1p-24f);
   const uint32_t k1t = ts.rk1[0] ^ kTagElection;
   const uint32_t calls = (M + 3u) >> 2;
-  unsigned long long best = ((unsigned long long)0x3f800000u << 32) | 0xffffffffull;
+  float bestR = 1.0f;  // lane-local minimum; a lane sees its j in increasing order
+  uint32_t bestJ = 0xffffffffu;
   for (uint32_t c = lane; c < calls; c += 32u) {
     const Philox4 x = ts.with_tag(c, sel, k1t);
     const uint32_t xs[4] = {x.x, x.y, x.z, x.w};
@@ -71,9 +72,13 @@ __device__ __forceinline__ void row_argmin(const Stream& ts, uint32_t sel, uint3
       const float d = j < M ? lds_f32(row_s + 4u * j) : 0.f;
       const float t = scaled_u<FOLD>(xs[q], T, T_s);
       const float R = (t < d) ? __fdiv_rn(t, d) : 1.0f;
-      best = min(best, ((unsigned long long)__float_as_uint(R) << 32) | j);
+      if (R < bestR) {
+        bestR = R;
+        bestJ = j;
+      }
     }
   }
+  unsigned long long best = ((unsigned long long)__float_as_uint(bestR) << 32) | bestJ;
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) best = min(best, __shfl_xor_sync(kFull, best, o));
   id = (uint32_t)(best >> 32) < 0x3f800000u ? (int32_t)(uint32_t)best : -1;
