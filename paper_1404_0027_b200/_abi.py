@@ -50,7 +50,8 @@ _lib = None
 
 
 def library_path() -> str:
-    return _build.LIBGPUAR
+    # GPUAR_LIBRARY: an alternative in-tree build (tuning experiments); default lib/libgpuar.so
+    return os.environ.get("GPUAR_LIBRARY", _build.LIBGPUAR)
 
 
 def load() -> ctypes.CDLL:

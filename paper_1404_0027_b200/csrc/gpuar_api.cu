@@ -56,6 +56,9 @@ struct gpuar_handle {
   // device scratch
   DevStats* d_stats = nullptr;
   DevCounters* d_ctr = nullptr;
+  uint32_t ticket_phase = 0;  // DevCounters::next set of the next shared-vector launch
+  uint32_t grab_override = 0; // tuning knobs, read from the environment once at create time
+  uint32_t no_prefetch = 0;
   double* d_part_sum = nullptr;
   uint32_t* d_part_max = nullptr;
   int stats_blocks = 1;
@@ -98,14 +101,15 @@ struct gpuar_handle {
 namespace {
 
 struct DeviceGuard {
+  int dev;
   int prev = -1;
   bool ok = true;
-  explicit DeviceGuard(int dev) {
+  explicit DeviceGuard(int d) : dev(d) {
     if (cudaGetDevice(&prev) != cudaSuccess) prev = -1;
     if (prev != dev) ok = cudaSetDevice(dev) == cudaSuccess;
   }
-  ~DeviceGuard() {
-    if (prev >= 0) cudaSetDevice(prev);
+  ~DeviceGuard() {  // restore only what was switched
+    if (prev >= 0 && prev != dev) cudaSetDevice(prev);
   }
 };
 
@@ -138,10 +142,12 @@ void plan_shared(gpuar_handle* h) {
     h->n_pref = (uint32_t)((M + (1ull << s) - 1) >> s);
     h->shared_smem = (uint32_t)(((2u * h->n_pref + 15u) & ~15ull) + 16u);
   }
-  // block size maximising resident threads per SM
+  // block size maximising resident threads per SM (GPUAR_SH_CTAS_PER_SM: fewer CTAs, tuning)
   int best_threads = 0;
+  const int cap = env_int("GPUAR_SH_CTAS_PER_SM", 0);
   for (int block : {256, 512, 1024}) {
-    const int n = select_shared_blocks_per_sm(h->shared_path, block, h->shared_smem);
+    int n = select_shared_blocks_per_sm(h->shared_path, block, h->shared_smem);
+    if (cap > 0) n = std::min(n, cap);
     if (n * block > best_threads) {
       best_threads = n * block;
       h->sh_block = block;
@@ -199,8 +205,8 @@ int launch_select(gpuar_handle* h, const float* alpha, int64_t rows, int64_t ld,
     p.group_shift = h->group_shift;
     p.smem_bytes = h->shared_smem;
     p.w = h->w;
-    p.grab_override = (uint32_t)std::max(0, env_int("GPUAR_GRAB", 0));
-    p.no_prefetch = (uint32_t)env_int("GPUAR_NO_PREFETCH", 0);
+    p.grab_override = h->grab_override;
+    p.no_prefetch = h->no_prefetch;
     if (h->rule == kRuleArgmin) {
       e = launch_argmin_shared(p, h->am_smem, h->am_grid, 256, st);
     } else if (h->rule == kRuleIT) {
@@ -212,8 +218,11 @@ int launch_select(gpuar_handle* h, const float* alpha, int64_t rows, int64_t ld,
       }
       const bool smem = (size_t)h->M * 8u + 1024u <= (size_t)h->smem_optin;
       if (e == cudaSuccess) e = launch_it_select(p, h->d_prefix, smem, h->num_sms * 8, st);
-    } else
+    } else {
+      p.phase = h->ticket_phase;
       e = launch_select_shared(p, h->shared_path, h->sh_grid, h->sh_block, st);
+      if (e == cudaSuccess) h->ticket_phase ^= 1u;
+    }
   } else {
     RowsParams p{};
     p.alpha = alpha;
@@ -311,6 +320,8 @@ int gpuar_create(gpuar_t* out, int64_t M, int64_t K, uint64_t seed) {
   // stats launch shape depends on M only -> identical reduction tree on every rank
   h->stats_blocks = (int)std::min<int64_t>((M + 4095) / 4096, 512);
   plan_shared(h);
+  h->grab_override = (uint32_t)std::max(0, env_int("GPUAR_GRAB", 0));
+  h->no_prefetch = (uint32_t)std::max(0, env_int("GPUAR_NO_PREFETCH", 0));
   cudaError_t e = cudaMalloc(&h->d_stats, sizeof(DevStats));
   if (e == cudaSuccess) e = cudaMalloc(&h->d_ctr, sizeof(DevCounters));
   if (e == cudaSuccess) e = cudaMalloc(&h->d_part_sum, sizeof(double) * h->stats_blocks);

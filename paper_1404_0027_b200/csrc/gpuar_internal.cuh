@@ -24,8 +24,10 @@ struct DevStats {
 // Per-handle device counters.
 constexpr uint32_t kStripes = 64;  // work-stealing tickets, one per stripe of selections
 struct DevCounters {
-  unsigned long long next[kStripes];  // tickets (reset by the last CTA of each launch)
-  unsigned int done;                  // CTAs finished in the current launch
+  // Tickets, double-buffered: launch n of the shared-vector kernel uses set n & 1 and zeroes
+  // set (n + 1) & 1 for the next launch (the launch before it, which used that set, has
+  // completed in stream order) -- no end-of-launch counter or fence.
+  unsigned long long next[2][kStripes];
   unsigned int err;                   // sticky EPROPENSITY flag (cleared by the host)
 };
 
@@ -63,6 +65,7 @@ struct SharedParams {
   float w;                   // argmin rule: T = fl32(w * alpha_max)
   uint32_t grab_override;    // tuning: fixed selections per ticket grab (0 = model)
   uint32_t no_prefetch;      // tuning: 1 = fetch tickets on demand
+  uint32_t phase;            // ticket set of this launch (DevCounters::next)
 };
 
 struct RowsParams {
@@ -169,24 +172,32 @@ __device__ __forceinline__ void bulk_g2s_plain(void* dst, const void* src, uint3
 }
 
 // Stage `nbytes` at global `src` into this CTA's shared memory at `dst` (16-byte aligned)
-// with bulk async copies of the 16-byte-aligned hull; returns the shared address of the
-// first byte of src.  Every thread of the CTA must call it (it synchronises the CTA).
-__device__ __forceinline__ uint32_t stage_to_smem(unsigned char* dst, const void* src, uint32_t nbytes, uint64_t* bar) {
+// with bulk async copies of the 16-byte-aligned hull, in two halves so that the copy
+// overlaps other work: stage_issue (thread 0 initialises the mbarrier and issues the
+// copies; every thread gets the shared address of the first byte of src), then, after a
+// __syncthreads that publishes the barrier's initialisation, stage_wait by every thread.
+__device__ __forceinline__ uint32_t stage_issue(unsigned char* dst, const void* src, uint32_t nbytes, uint64_t* bar) {
   const uintptr_t a = reinterpret_cast<uintptr_t>(src);
   const uintptr_t lo = a & ~(uintptr_t)15;
   const uint32_t total = (uint32_t)(((a + nbytes + 15u) & ~(uintptr_t)15) - lo);
   if (threadIdx.x == 0) {
     mbar_init(bar, 1u);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-  }
-  __syncthreads();
-  if (threadIdx.x == 0) {
     mbar_arrive_expect_tx(bar, total);
     for (uint32_t off = 0; off < total; off += 32768u)
       bulk_g2s_plain(dst + off, reinterpret_cast<const unsigned char*>(lo) + off, min(32768u, total - off), bar);
   }
-  mbar_wait(bar, 0u);
   return smem_u32(dst) + (uint32_t)(a - lo);
+}
+
+__device__ __forceinline__ void stage_wait(uint64_t* bar) { mbar_wait(bar, 0u); }
+
+// Both halves at once.  Every thread of the CTA must call it (it synchronises the CTA).
+__device__ __forceinline__ uint32_t stage_to_smem(unsigned char* dst, const void* src, uint32_t nbytes, uint64_t* bar) {
+  const uint32_t s = stage_issue(dst, src, nbytes, bar);
+  __syncthreads();
+  stage_wait(bar);
+  return s;
 }
 
 __device__ __forceinline__ void fence_proxy_async_smem() {

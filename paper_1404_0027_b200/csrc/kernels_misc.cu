@@ -91,8 +91,7 @@ __global__ void __launch_bounds__(kStatsThreads) stats_pass2(const double* part_
     s.grab = grab;
     s.pad = 0;
     *stats = s;
-    for (uint32_t i = 0; i < kStripes; ++i) ctr->next[i] = 0ull;
-    ctr->done = 0u;
+    for (uint32_t i = 0; i < kStripes; ++i) ctr->next[0][i] = ctr->next[1][i] = 0ull;
     if (!s.valid) atomicOr(&ctr->err, 1u);
   }
 }

@@ -57,18 +57,19 @@ struct Pool {
   unsigned long long next, end;  // current chunk [next, end)
   unsigned long long grab, first;
   unsigned long long pending;    // lane 0: ticket of the NEXT chunk, fetched one chunk ahead
+  unsigned long long* tickets;   // this launch's ticket set (DevCounters::next[phase])
   uint32_t K, nwarps, stripe;
   bool exhausted;
 
   // Lane 0 issues the atomic for the chunk after the current one; its latency (~1 us under
   // contention) overlaps the current chunk's work instead of stalling the warp.
   bool ahead;                    // prefetch one chunk ahead (else fetch on demand)
-  __device__ __forceinline__ void prefetch(DevCounters* ctr, uint32_t lane) {
-    if (lane == 0u) pending = dyn_base(stripe) + atomicAdd(&ctr->next[stripe], grab);
+  __device__ __forceinline__ void prefetch(uint32_t lane) {
+    if (lane == 0u) pending = dyn_base(stripe) + atomicAdd(&tickets[stripe], grab);
   }
   // Move to the prefetched chunk (and prefetch the one after); false when the stripe is done.
-  __device__ __forceinline__ bool refill(DevCounters* ctr, uint32_t lane) {
-    if (!ahead) prefetch(ctr, lane);
+  __device__ __forceinline__ bool refill(uint32_t lane) {
+    if (!ahead) prefetch(lane);
     const unsigned long long b = __shfl_sync(kFull, pending, 0);
     const unsigned long long hi = stripe_hi(stripe);
     if (b >= hi) {
@@ -77,7 +78,7 @@ struct Pool {
     }
     next = b;
     end = min(b + grab, hi);
-    if (ahead) prefetch(ctr, lane);
+    if (ahead) prefetch(lane);
     return true;
   }
 
@@ -94,9 +95,10 @@ struct Pool {
 };
 
 __device__ __forceinline__ void pool_init(Pool& pl, uint32_t K, uint32_t nwarps, uint32_t warp_global,
-                                          unsigned long long first, unsigned long long grab, DevCounters* ctr,
-                                          bool ahead) {
+                                          unsigned long long first, unsigned long long grab,
+                                          unsigned long long* tickets, bool ahead) {
   pl.ahead = ahead;
+  pl.tickets = tickets;
   pl.K = K;
   pl.nwarps = nwarps;
   pl.first = first;
@@ -109,16 +111,15 @@ __device__ __forceinline__ void pool_init(Pool& pl, uint32_t K, uint32_t nwarps,
   // nothing static and no dynamic part left in the stripe: done without touching the ticket
   pl.exhausted = pl.next >= pl.end && pl.dyn_base(pl.stripe) >= hi;
   pl.pending = ~0ull;
-  if (ahead && pl.dyn_base(pl.stripe) < hi) pl.prefetch(ctr, threadIdx.x & 31u);
+  if (ahead && pl.dyn_base(pl.stripe) < hi) pl.prefetch(threadIdx.x & 31u);
 }
 
 // Hand idle teams (leader lanes in `need`) the next selections of the warp's pool.
 // Returns the new selection of this lane's team (broadcast from its leader) or kNone.
-__device__ __forceinline__ uint32_t pool_take(Pool& pl, uint32_t need, uint32_t lane, uint32_t tbase,
-                                              DevCounters* ctr) {
+__device__ __forceinline__ uint32_t pool_take(Pool& pl, uint32_t need, uint32_t lane, uint32_t tbase) {
   uint32_t got = kNone;
   while (need != 0u && !pl.exhausted) {
-    if (pl.next >= pl.end && !pl.refill(ctr, lane)) break;
+    if (pl.next >= pl.end && !pl.refill(lane)) break;
     const uint32_t avail = (uint32_t)(pl.end - pl.next);
     const uint32_t r = __popc(need & lanemask_lt());
     uint32_t mine = kNone;
@@ -156,7 +157,7 @@ __device__ __forceinline__ void trial_loop(const SharedParams& P, const TrialStr
   while (true) {
     const uint32_t need = __ballot_sync(kFull, leader && my == kNone);
     if (need != 0u) {
-      const uint32_t got = pool_take(pl, need, lane, tbase, P.ctr);
+      const uint32_t got = pool_take(pl, need, lane, tbase);
       if (got != kNone) {
         my = got;
         sel = ts.sel_word(P.s0 + got);
@@ -224,7 +225,7 @@ __device__ __forceinline__ void lane_loop(const SharedParams& P, const TrialStre
   while (true) {
     if (need != 0u) {  // warp-uniform: hand out selections
       while (need != 0u && !pl.exhausted) {
-        if (pl.next >= pl.end && !pl.refill(P.ctr, lane)) break;
+        if (pl.next >= pl.end && !pl.refill(lane)) break;
         const uint32_t avail = (uint32_t)(pl.end - pl.next);
         const uint32_t r = __popc(need & lt);
         const bool mine = ((need >> lane) & 1u) && r < avail;
@@ -269,7 +270,7 @@ __device__ __forceinline__ void warp_loop(const SharedParams& P, const TrialStre
   const uint32_t calls = half + (P.max_trials & 1u);
   const uint32_t lane = threadIdx.x & 31u;
   while (!pl.exhausted) {
-    if (pl.next >= pl.end && !pl.refill(P.ctr, lane)) break;
+    if (pl.next >= pl.end && !pl.refill(lane)) break;
     const uint32_t my = (uint32_t)pl.next++;
     const uint32_t sel = ts.sel_word(P.s0 + my);
     int32_t id = -1;
@@ -326,14 +327,26 @@ __device__ __forceinline__ uint32_t choose_team(float p, uint32_t K, uint32_t nw
 template <int PATH>
 __global__ void __launch_bounds__(1024, 1) select_shared_kernel(const SharedParams P) {
   extern __shared__ __align__(16) unsigned char smem[];
+  __shared__ uint64_t stage_bar;
+  __shared__ uint32_t s_g;
+  // the next launch's ticket set (its previous user, launch n - 1, has completed)
+  if (blockIdx.x == 0 && threadIdx.x < kStripes) P.ctr->next[P.phase ^ 1u][threadIdx.x] = 0ull;
+  // ---- stage the vector (path 1) or its prefilter (paths 2, 3) in smem with one bulk async
+  // copy per CTA (16-byte hull; the data starts `sbase` bytes into it), issued first so that
+  // it overlaps the statistics load and the tau phase
+  const uint32_t sbase = (PATH == kPathSmemF32) ? stage_issue(smem, P.alpha, 4u * P.M, &stage_bar)
+                                                : stage_issue(smem, P.prefilter, 2u * P.n_pref, &stage_bar);
   const DevStats st = *P.stats;
   const uint32_t tid = blockIdx.x * blockDim.x + threadIdx.x;
   const uint32_t nthreads = gridDim.x * blockDim.x;
   const bool invalid = st.valid == 0u;
   const bool zero = st.amax_bits == 0u;
+  const uint32_t K = P.K;
+  const uint32_t nwarps = nthreads >> 5;
+  if (threadIdx.x == 0) s_g = choose_team(st.p, K, nwarps);  // once per CTA, not per warp
 
   // ---- phase A: tau for every selection; degenerate / invalid outputs
-  for (uint32_t s = tid; s < P.K; s += nthreads) {
+  for (uint32_t s = tid; s < K; s += nthreads) {
     if (invalid || zero) {
       P.idx[s] = -1;
       if (P.trials) P.trials[s] = 0u;
@@ -342,22 +355,13 @@ __global__ void __launch_bounds__(1024, 1) select_shared_kernel(const SharedPara
       P.tau[s] = __fdiv_rn(neg_log_u1(P.seed_lo, P.seed_hi, P.s0 + s, P.epoch), st.a0f);
     }
   }
-  if (invalid || zero) return;  // uniform over the grid; the pool counter is untouched
-
-  // ---- phase B: stage the vector (path 1) or its prefilter (paths 2, 3) in smem with one
-  // bulk async copy per CTA (16-byte hull; the data starts `sbase` bytes into it)
-  __shared__ uint64_t stage_bar;
-  const uint32_t sbase = (PATH == kPathSmemF32) ? stage_to_smem(smem, P.alpha, 4u * P.M, &stage_bar)
-                                                : stage_to_smem(smem, P.prefilter, 2u * P.n_pref, &stage_bar);
+  __syncthreads();        // publishes the barrier's initialisation and s_g
+  stage_wait(&stage_bar);  // (also before an early exit: no copy may outlive the CTA)
+  if (invalid || zero) return;  // uniform over the grid; the tickets are untouched
 
   // ---- phase C: trials
   const float amax = __uint_as_float(st.amax_bits);
-  const uint32_t K = P.K;
-  const uint32_t nwarps = nthreads >> 5;
   const uint32_t warp_global = tid >> 5;
-  __shared__ uint32_t s_g;
-  if (threadIdx.x == 0) s_g = choose_team(st.p, K, nwarps);  // once per CTA, not per warp
-  __syncthreads();
   const uint32_t g = s_g;
   // static first chunk: half of a warp's fair share; then grabs of ~8192 expected trials
   // (st.grab), at most an eighth of the fair share (but two teams' worth), at least one
@@ -369,7 +373,7 @@ __global__ void __launch_bounds__(1024, 1) select_shared_kernel(const SharedPara
   unsigned long long grab = max(teams, min((unsigned long long)st.grab, max(2ull * teams, fair / 8ull)));
   if (P.grab_override) grab = P.grab_override;
   Pool pl;
-  pool_init(pl, K, nwarps, warp_global, first, grab, P.ctr, P.no_prefetch == 0u);
+  pool_init(pl, K, nwarps, warp_global, first, grab, P.ctr->next[P.phase], P.no_prefetch == 0u);
   const TrialStream ts(P.seed_lo, P.seed_hi, P.epoch);
   const bool fold = can_fold(st.amax_bits);
   if (g == 1u) {
@@ -387,18 +391,6 @@ __global__ void __launch_bounds__(1024, 1) select_shared_kernel(const SharedPara
       trial_loop<PATH, true>(P, ts, sbase, amax, g, pl);
     else
       trial_loop<PATH, false>(P, ts, sbase, amax, g, pl);
-  }
-
-  // ---- the last CTA out resets the work-stealing ticket for the next launch
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    __threadfence();
-    const unsigned int prev = atomicAdd(&P.ctr->done, 1u);
-    if (prev == gridDim.x - 1u) {
-      for (uint32_t i = 0; i < kStripes; ++i) P.ctr->next[i] = 0ull;
-      P.ctr->done = 0u;
-      __threadfence();
-    }
   }
 }
 

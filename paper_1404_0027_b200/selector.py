@@ -45,6 +45,7 @@ class Selector:
         self._h = h
         self._alpha = None      # keeps the borrowed propensity tensor alive
         self._rows = 0
+        self._last_stream = None
 
     # ----------------------------------------------------------------- lifecycle
     def close(self) -> None:
@@ -66,7 +67,9 @@ class Selector:
 
     def _stream(self) -> None:
         s = torch.cuda.current_stream(self.device).cuda_stream
-        check(self._lib.gpuar_set_stream(self._h, ctypes.c_void_p(s)), "gpuar_set_stream")
+        if s != self._last_stream:  # gpuar_set_stream orders the new stream after the old one
+            check(self._lib.gpuar_set_stream(self._h, ctypes.c_void_p(s)), "gpuar_set_stream")
+            self._last_stream = s
 
     # ----------------------------------------------------------------- state
     @property
@@ -132,9 +135,9 @@ class Selector:
             trials = torch.empty(K, dtype=torch.int32, device=self.device) if with_trials else None
         else:
             idx, tau, trials = out
-        with torch.cuda.device(self.device):
-            self._stream()
-            check(self._lib.gpuar_select(self._h, K, _ptr(idx), _ptr(tau), _ptr(trials)), "gpuar_select")
+        # (no torch device context: the library switches to the handle's device itself)
+        self._stream()
+        check(self._lib.gpuar_select(self._h, K, _ptr(idx), _ptr(tau), _ptr(trials)), "gpuar_select")
         return idx, tau, trials
 
     def select_host(self, alpha: np.ndarray | torch.Tensor, K: int | None = None, out: tuple | None = None):
