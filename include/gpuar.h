@@ -64,7 +64,7 @@ typedef struct gpuar_handle *gpuar_t;
 
 /* Create a selector for M reactions and up to K selections per gpuar_select call.
  * Allocates the handle's device scratch (statistics, counters, large-M prefilter) on the
- * current device.  epoch = 0, selection offset = 0, max_trials = 2^20, stream = 0.
+ * current device (the shared-vector thresholds are allocated by gpuar_set_propensities).  epoch = 0, selection offset = 0, max_trials = 2^20, stream = 0.
  * M in [1, 2^31-1], K in [1, 2^32-1].  Errors: EINVAL, ENOMEM, ECUDA.  *out is set only on
  * success. */
 int gpuar_create(gpuar_t *out, int64_t M, int64_t K, uint64_t seed);
@@ -82,15 +82,17 @@ int gpuar_set_stream(gpuar_t h, void *stream);
 /* Register the propensities (device pointer, binary32, BORROWED).
  *   rows == 1 : one shared M-vector for every selection (configs c1/c2/c3/c5); enqueues
  *               the statistics pass (alpha_max exact, alpha_0 summed in binary64 with a
- *               fixed tree, validity) and, for M beyond the shared-memory capacity, the
- *               exact shared-memory prefilter.  The pointer is kept: call again after
- *               mutating the buffer.  ld is ignored (pass M).
+ *               fixed tree, validity), then the classic rule's acceptance thresholds
+ *               T_j (R22; M words of handle scratch, allocated on the first
+ *               shared vector: ENOMEM) and, for M beyond the shared-memory capacity, their
+ *               exact 16-bit shared-memory prefilter.  The pointer is kept: call again
+ *               after mutating the buffer.  ld is ignored (pass M).
  *   rows == K : per-realization matrix, row r (pitch ld >= M floats, row-major
  *               D[r*ld + j]) belongs to local selection r; its
  *               alpha_max / alpha_0 are reduced inside gpuar_select.  d_alpha must be
  *               16-byte aligned (rows are streamed with 1-D bulk async copies).
- * Errors: EINVAL (NULL pointer, rows not in {1, K}, ld < M, misaligned matrix base).
- * Invalid values are reported later as sticky EPROPENSITY. */
+ * Errors: EINVAL (NULL pointer, rows not in {1, K}, ld < M, misaligned matrix base),
+ * ENOMEM, ECUDA.  Invalid values are reported later as sticky EPROPENSITY. */
 int gpuar_set_propensities(gpuar_t h, const float *d_alpha, int64_t rows, int64_t ld);
 
 /* Select for local s in [0, K): global index s_g = offset + s, current epoch.  Writes
@@ -193,9 +195,10 @@ int gpuar_histogram(gpuar_t h, const int32_t *d_idx, const uint32_t *d_trials, i
  * handle's stream, folding the outputs into d_sink[thread].  Asynchronous. */
 int gpuar_bench_philox(gpuar_t h, int64_t n_threads, int32_t calls, uint32_t *d_sink);
 
-/* Which selection kernel the current registration uses (0 none, 1 shared vector in
- * shared memory, 2 shared vector with the per-element bf16 prefilter, 3 shared vector
- * with the group-max prefilter, 4 per-realization rows).  Pure host query. */
+/* Which selection kernel the current registration uses (0 none, 1 shared vector: its
+ * acceptance thresholds all in shared memory, 2 shared vector: per-element 16-bit threshold
+ * brackets in shared memory, 3 shared vector: per-group 16-bit threshold bounds in shared
+ * memory, 4 per-realization rows).  Pure host query. */
 int gpuar_path(gpuar_t h, int32_t *path);
 
 /* Static text for a status code. */

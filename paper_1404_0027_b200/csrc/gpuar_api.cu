@@ -16,7 +16,7 @@ using namespace gpuar;
 
 namespace {
 
-constexpr int kRowsMaxWarps = 32;      // compiled variants: <=16, <=24, <=32 warps per CTA
+constexpr int kRowsMaxWarps = 32;      // compiled variants: <=16, <=20, <=24, <=32 warps per CTA
 constexpr int kRowsDefaultWarps = 24;   // r01 sweep: 24 warps x 2 slots -> 5.92 TB/s (16x3: 5.13)
 constexpr size_t kHostChunkBytes = 64ull << 20;  // gpuar_select_host row-chunk size
 
@@ -63,6 +63,7 @@ struct gpuar_handle {
   uint32_t* d_part_max = nullptr;
   int stats_blocks = 1;
   uint16_t* d_pref = nullptr;
+  uint32_t* d_thr = nullptr;  // classic-rule acceptance thresholds T_j of the shared vector
   uint32_t n_pref = 0, group_shift = 0;
   int shared_path = kPathSmemF32;  // which shared-vector path M implies
   uint32_t shared_smem = 0;
@@ -188,6 +189,7 @@ int launch_select(gpuar_handle* h, const float* alpha, int64_t rows, int64_t ld,
   if (rows == 1) {
     SharedParams p{};
     p.alpha = alpha;
+    p.thr = h->d_thr;
     p.prefilter = h->d_pref;
     p.stats = h->d_stats;
     p.ctr = h->d_ctr;
@@ -265,10 +267,15 @@ int check_err_flag(gpuar_handle* h) {
 }
 
 int register_shared(gpuar_handle* h, const float* d_alpha) {
+  if (!h->d_thr) {  // first shared vector of this handle: M acceptance thresholds
+    const cudaError_t a = cudaMalloc(&h->d_thr, (sizeof(uint32_t) * (size_t)h->M + 15u) & ~(size_t)15);
+    if (a != cudaSuccess) return cuda_status(a);
+  }
   cudaError_t e = launch_stats(d_alpha, (uint32_t)h->M, h->d_part_sum, h->d_part_max, h->d_stats, h->d_ctr,
                                h->stats_blocks, h->stream);
-  if (e == cudaSuccess && h->shared_path != kPathSmemF32)
-    e = launch_prefilter(d_alpha, (uint32_t)h->M, h->d_pref, h->n_pref, h->group_shift, h->shared_path, h->stream);
+  if (e == cudaSuccess)
+    e = launch_thresholds(d_alpha, (uint32_t)h->M, h->d_stats, h->d_thr, h->d_pref, h->n_pref, h->group_shift,
+                          h->shared_path, h->stream);
   if (e != cudaSuccess) return cuda_status(e);
   h->alpha = d_alpha;
   h->rows = 1;
@@ -361,6 +368,7 @@ int gpuar_destroy(gpuar_t h) {
   cudaFree(h->d_part_sum);
   cudaFree(h->d_part_max);
   cudaFree(h->d_pref);
+  cudaFree(h->d_thr);
   cudaFree(h->d_prefix);
   if (h->order_ev) cudaEventDestroy(h->order_ev);
   cudaFree(h->d_dep_ptr);

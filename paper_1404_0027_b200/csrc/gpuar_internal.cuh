@@ -33,9 +33,9 @@ struct DevCounters {
 
 enum Path : int {
   kPathNone = 0,
-  kPathSmemF32 = 1,    // shared vector fully in shared memory (binary32)
-  kPathSmemBf16 = 2,   // shared vector: per-element bf16 truncation bracket in smem, exact in L2
-  kPathSmemGroup = 3,  // shared vector: bf16 round-up group maxima in smem, exact in L2
+  kPathSmemF32 = 1,    // shared vector: its acceptance thresholds T_j (32-bit) all in shared memory
+  kPathSmemBf16 = 2,   // shared vector: 16-bit threshold brackets in smem, exact T_j in L2
+  kPathSmemGroup = 3,  // shared vector: 16-bit group bounds of T_j in smem, exact T_j in L2
   kPathRows = 4,       // per-realization K x M matrix, bulk-async staged rows
 };
 
@@ -47,7 +47,8 @@ enum Rule : int {
 
 struct SharedParams {
   const float* alpha;        // M floats (device)
-  const uint16_t* prefilter; // paths 2/3: bf16 codes (device)
+  const uint32_t* thr;       // classic rule: acceptance thresholds T_j (device, M words)
+  const uint16_t* prefilter; // paths 2/3: 16-bit threshold brackets / group bounds (device)
   const DevStats* stats;
   DevCounters* ctr;
   int32_t* idx;
@@ -256,8 +257,8 @@ __device__ __forceinline__ uint32_t lanemask_lt() {
 
 cudaError_t launch_stats(const float* alpha, uint32_t M, double* part_sum, uint32_t* part_max,
                          DevStats* stats, DevCounters* ctr, int stats_blocks, cudaStream_t st);
-cudaError_t launch_prefilter(const float* alpha, uint32_t M, uint16_t* pref, uint32_t n_pref,
-                             uint32_t group_shift, int path, cudaStream_t st);
+cudaError_t launch_thresholds(const float* alpha, uint32_t M, const DevStats* stats, uint32_t* thr, uint16_t* pref,
+                              uint32_t n_pref, uint32_t group_shift, int path, cudaStream_t st);
 cudaError_t launch_select_shared(const SharedParams& p, int path, int grid, int block, cudaStream_t st);
 cudaError_t launch_argmin_shared(const SharedParams& p, bool smem, int grid, int block, cudaStream_t st);
 void set_argmin_limits(int bytes);

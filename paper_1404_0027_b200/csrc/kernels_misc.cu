@@ -96,22 +96,53 @@ __global__ void __launch_bounds__(kStatsThreads) stats_pass2(const double* part_
   }
 }
 
-// Path 2: per-element bf16 truncation t_j = bits(alpha_j) >> 16, so that
-// bf16(t_j) <= alpha_j < bf16(t_j + 1).  Path 3: per-group bf16 round-up of the group
-// maximum, an upper bound of every alpha_j in the group.
-__global__ void prefilter_kernel(const float* __restrict__ alpha, uint32_t M, uint16_t* pref, uint32_t n_pref,
-                                 uint32_t group_shift, int path) {
-  for (uint32_t g = blockIdx.x * blockDim.x + threadIdx.x; g < n_pref; g += gridDim.x * blockDim.x) {
-    if (path == kPathSmemBf16) {
-      pref[g] = (uint16_t)(__float_as_uint(__ldg(alpha + g)) >> 16);
-    } else {
+// Acceptance threshold (R22).  The classic test on candidate j accepts the 24-bit
+// uniform v = x >> 8 iff fl32(fl32(v 2^-24) alpha_max) < alpha_j (with
+// u = v 2^-24 exact).  v -> fl32(v 2^-24 alpha_max) is non-decreasing (an exact scaling
+// followed by one round-to-nearest multiply by alpha_max >= 0), so the accepted v form a
+// prefix [0, T_j): T_j = min{v in [0, 2^24] : v = 2^24 or fl32(fl32(v 2^-24) alpha_max) >=
+// alpha_j}, found by bisection on exactly that expression.  The trial then tests the
+// integer v < T_j: bit-identical decisions, no int->float conversion or multiply per trial.
+__device__ __forceinline__ uint32_t accept_threshold(float alpha_j, float amax) {
+  uint32_t lo = 0u, hi = 1u << 24;  // answer in [lo, hi]
+  while (lo < hi) {
+    const uint32_t mid = (lo + hi) >> 1;
+    if (__fmul_rn(__fmul_rn(__uint2float_rn(mid), 0x1p-24f), amax) >= alpha_j)
+      hi = mid;
+    else
+      lo = mid + 1u;
+  }
+  return lo;
+}
+
+// T_j for every reaction, plus the shared-memory prefilter of paths 2 and 3:
+//  path 2: B_j = min(T_j >> 8, 65535), so that (x >> 16) < B_j accepts, (x >> 16) > B_j
+//          rejects, and only (x >> 16) == B_j (probability 2^-16) needs the exact T_j;
+//  path 3: per group of 2^group_shift reactions G_g = min(ceil(max T_j / 256), 65535), so that
+//          (x >> 16) > G_g rejects every j of the group; otherwise the exact T_j decides.
+__global__ void thresholds_kernel(const float* __restrict__ alpha, uint32_t M, const DevStats* __restrict__ stats,
+                                  uint32_t* thr, uint16_t* pref, uint32_t n_pref, uint32_t group_shift, int path) {
+  const DevStats st = *stats;
+  if (!st.valid) return;  // the select kernels stop on invalid statistics
+  const float amax = __uint_as_float(st.amax_bits);
+  const uint32_t stride = gridDim.x * blockDim.x;
+  if (path != kPathSmemGroup) {
+    for (uint32_t j = blockIdx.x * blockDim.x + threadIdx.x; j < M; j += stride) {
+      const uint32_t t = accept_threshold(__ldg(alpha + j), amax);
+      thr[j] = t;
+      if (path == kPathSmemBf16) pref[j] = (uint16_t)min(t >> 8, 65535u);
+    }
+  } else {
+    for (uint32_t g = blockIdx.x * blockDim.x + threadIdx.x; g < n_pref; g += stride) {
       const uint32_t lo = g << group_shift;
       const uint32_t hi = min(M, lo + (1u << group_shift));
       uint32_t mx = 0;
-      for (uint32_t j = lo; j < hi; ++j) mx = max(mx, __float_as_uint(__ldg(alpha + j)));
-      // round up to bf16; saturates to +inf (0x7f80), still an upper bound
-      const uint32_t up = mx >= 0x7f7f0001u ? 0x7f80u : ((mx + 0xffffu) >> 16);
-      pref[g] = (uint16_t)up;
+      for (uint32_t j = lo; j < hi; ++j) {
+        const uint32_t t = accept_threshold(__ldg(alpha + j), amax);
+        thr[j] = t;
+        mx = max(mx, t);
+      }
+      pref[g] = (uint16_t)min((mx + 255u) >> 8, 65535u);
     }
   }
 }
@@ -174,11 +205,12 @@ cudaError_t launch_stats(const float* alpha, uint32_t M, double* part_sum, uint3
   return cudaGetLastError();
 }
 
-cudaError_t launch_prefilter(const float* alpha, uint32_t M, uint16_t* pref, uint32_t n_pref, uint32_t group_shift,
-                             int path, cudaStream_t st) {
+cudaError_t launch_thresholds(const float* alpha, uint32_t M, const DevStats* stats, uint32_t* thr, uint16_t* pref,
+                              uint32_t n_pref, uint32_t group_shift, int path, cudaStream_t st) {
   const int block = 256;
-  const int grid = (int)std::min<uint32_t>((n_pref + block - 1) / block, 4096u);
-  prefilter_kernel<<<grid, block, 0, st>>>(alpha, M, pref, n_pref, group_shift, path);
+  const uint32_t n = path == kPathSmemGroup ? n_pref : M;
+  const int grid = (int)std::min<uint32_t>((n + block - 1) / block, 4096u);
+  thresholds_kernel<<<grid, block, 0, st>>>(alpha, M, stats, thr, pref, n_pref, group_shift, path);
   return cudaGetLastError();
 }
 

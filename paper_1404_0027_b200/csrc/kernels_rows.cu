@@ -315,6 +315,7 @@ cudaError_t launch_select_rows(const RowsParams& p, int grid, int warps, cudaStr
   const size_t S = (size_t)1 << p.log2_stages;
   const size_t sh = (((size_t)warps * S * 8u + 127u) & ~(size_t)127u) + (size_t)warps * S * p.stage_bytes;
   if (warps <= 16) return launch_w<16>(p, grid, warps, sh, st);
+  if (warps <= 20) return launch_w<20>(p, grid, warps, sh, st);
   if (warps <= 24) return launch_w<24>(p, grid, warps, sh, st);
   return launch_w<32>(p, grid, warps, sh, st);
 }
@@ -324,6 +325,8 @@ int select_rows_blocks_per_sm(int warps, size_t smem) {
   cudaError_t e;
   if (warps <= 16)
     e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, select_rows_kernel<16, kRuleClassic>, warps * 32, smem);
+  else if (warps <= 20)
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, select_rows_kernel<20, kRuleClassic>, warps * 32, smem);
   else if (warps <= 24)
     e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, select_rows_kernel<24, kRuleClassic>, warps * 32, smem);
   else
@@ -333,6 +336,7 @@ int select_rows_blocks_per_sm(int warps, size_t smem) {
 
 void set_select_rows_limits(int bytes) {
   set_limits_w<16>(bytes);
+  set_limits_w<20>(bytes);
   set_limits_w<24>(bytes);
   set_limits_w<32>(bytes);
 }

@@ -3,8 +3,9 @@
 // (PAPER.md:361-365), the first accepted trial winning (north_star; R6).
 //
 // Design (B200-first, not the paper's election/argmin kernels of PAPER.md:498-555):
-//  * one persistent launch; the vector (or an exact prefilter of it) is staged once per
-//    CTA in shared memory by one bulk async copy;
+//  * one persistent launch; the vector's acceptance thresholds T_j (or a 16-bit prefilter of
+//    them) are staged once per CTA in shared memory by one bulk async copy, so a trial is
+//    an integer compare (x >> 8) < T_j (R22);
 //  * a selection is worked by a TEAM of g lanes (g = 1..32, a power of two picked once per
 //    CTA from K and p by an instruction-count model): in round q lane `rank` makes Philox
 //    call c = q*g + rank, i.e. trials 2c and 2c+1, so a round covers the contiguous trial
@@ -24,26 +25,25 @@ namespace gpuar {
 
 namespace {
 
-// Exact acceptance test fl32(u*amax) < alpha_j on the shared-memory copy (path 1) or with
-// an exact prefilter (paths 2, 3).  `sbase` is the shared-state-space address of the
-// staged array (32-bit; no generic->shared conversion per gather).
+// The classic acceptance test fl32(u alpha_max) < alpha_j on the 24-bit
+// uniform v = x >> 8, as the integer test v < T_j with the thresholds of
+// kernels_misc.cu (R22).  Path 1: T_j from the shared-memory copy of the
+// threshold table.  Path 2: the 16-bit bracket B_j = min(T_j >> 8, 65535) decides unless
+// x >> 16 == B_j.  Path 3: x >> 16 above the group bound rejects; otherwise T_j from L2.
+// `sbase` is the shared-state-space address of the staged array.
 template <int PATH>
-__device__ __forceinline__ bool accept(float t, uint32_t j, uint32_t sbase, const float* __restrict__ alpha,
+__device__ __forceinline__ bool accept(uint32_t x, uint32_t j, uint32_t sbase, const uint32_t* __restrict__ thr,
                                        uint32_t group_shift) {
   if constexpr (PATH == kPathSmemF32) {
-    return t < lds_f32(sbase + 4u * j);
+    return (x >> 8) < lds_u32(sbase + 4u * j);
   } else if constexpr (PATH == kPathSmemBf16) {
-    // bf16(code) <= alpha_j < bf16(code + 1): decide without the exact value unless t
-    // falls inside that bracket (exact: DESIGN.md §5.2).
-    const uint32_t code = lds_u16(sbase + 2u * j);
-    const bool lo = t < __uint_as_float(code << 16);
-    const bool hi = t >= __uint_as_float((code + 1u) << 16);
-    if (lo | hi) return lo;
-    return t < __ldg(alpha + j);
+    const uint32_t b = lds_u16(sbase + 2u * j);
+    const uint32_t h = x >> 16;
+    if (h != b) return h < b;
+    return (x >> 8) < __ldg(thr + j);
   } else {
-    // group maximum rounded up to bf16 is an upper bound of alpha_j
-    if (t >= __uint_as_float(lds_u16(sbase + 2u * (j >> group_shift)) << 16)) return false;
-    return t < __ldg(alpha + j);
+    if ((x >> 16) > lds_u16(sbase + 2u * (j >> group_shift))) return false;
+    return (x >> 8) < __ldg(thr + j);
   }
 }
 
@@ -137,10 +137,9 @@ __device__ __forceinline__ uint32_t pool_take(Pool& pl, uint32_t need, uint32_t 
 // Trial phase of one warp with sub-warp teams (1 < g < 32 lanes per selection).
 // Fast path: one Philox call + two gathers + one vote per round; team bookkeeping only
 // when some team of the warp finished a selection.
-template <int PATH, bool FOLD>
-__device__ __forceinline__ void trial_loop(const SharedParams& P, const TrialStream& ts, uint32_t sbase, float amax,
-                                           uint32_t g, Pool pl) {
-  const float amax_s = __fmul_rn(amax, 0x1p-24f);
+template <int PATH>
+__device__ __forceinline__ void trial_loop(const SharedParams& P, const TrialStream& ts, uint32_t sbase, uint32_t g,
+                                           Pool pl) {
   const uint32_t M = P.M;
   const uint32_t half = P.max_trials >> 1;            // calls whose odd trial is < max_trials
   const uint32_t calls = half + (P.max_trials & 1u);  // calls whose even trial is < max_trials
@@ -173,11 +172,9 @@ __device__ __forceinline__ void trial_loop(const SharedParams& P, const TrialStr
       const Philox4 x = ts(c, sel);
       j0 = __umulhi(x.x, M);
       j1 = __umulhi(x.z, M);
-      const float t0 = scaled_u<FOLD>(x.y, amax, amax_s);
-      const float t1 = scaled_u<FOLD>(x.w, amax, amax_s);
       // branch-free: both gathers always issue (j < M is always a valid index)
-      const bool r0 = accept<PATH>(t0, j0, sbase, P.alpha, P.group_shift);
-      const bool r1 = accept<PATH>(t1, j1, sbase, P.alpha, P.group_shift);
+      const bool r0 = accept<PATH>(x.y, j0, sbase, P.thr, P.group_shift);
+      const bool r1 = accept<PATH>(x.w, j1, sbase, P.thr, P.group_shift);
       a0 = active & (c < calls) & r0;
       a1 = active & (c < half) & r1;
       ball = __ballot_sync(kFull, a0 || a1);
@@ -210,10 +207,8 @@ __device__ __forceinline__ void trial_loop(const SharedParams& P, const TrialStr
 // One lane per selection (g = 1, high p): every round each lane makes one Philox call for
 // its own selection; a lane that finishes stores its result and takes the next selection of
 // the warp's pool (one ballot + popc), with no cross-lane data exchange.
-template <int PATH, bool FOLD>
-__device__ __forceinline__ void lane_loop(const SharedParams& P, const TrialStream& ts, uint32_t sbase, float amax,
-                                          Pool pl) {
-  const float amax_s = __fmul_rn(amax, 0x1p-24f);
+template <int PATH>
+__device__ __forceinline__ void lane_loop(const SharedParams& P, const TrialStream& ts, uint32_t sbase, Pool pl) {
   const uint32_t M = P.M;
   const uint32_t half = P.max_trials >> 1;
   const uint32_t calls = half + (P.max_trials & 1u);
@@ -243,8 +238,8 @@ __device__ __forceinline__ void lane_loop(const SharedParams& P, const TrialStre
     const Philox4 x = ts(c, sel);
     const uint32_t j0 = __umulhi(x.x, M);
     const uint32_t j1 = __umulhi(x.z, M);
-    const bool r0 = accept<PATH>(scaled_u<FOLD>(x.y, amax, amax_s), j0, sbase, P.alpha, P.group_shift);
-    const bool r1 = accept<PATH>(scaled_u<FOLD>(x.w, amax, amax_s), j1, sbase, P.alpha, P.group_shift);
+    const bool r0 = accept<PATH>(x.y, j0, sbase, P.thr, P.group_shift);
+    const bool r1 = accept<PATH>(x.w, j1, sbase, P.thr, P.group_shift);
     const bool a0 = (c < calls) & r0;
     const bool a1 = (c < half) & r1;
     const bool done = active & (a0 | a1 | (c + 1u >= calls));
@@ -261,10 +256,8 @@ __device__ __forceinline__ void lane_loop(const SharedParams& P, const TrialStre
 // Whole-warp teams (g = 32): the warp works its selections one after another, 64 trials
 // per round, like the matrix kernel -- no per-round team bookkeeping, ~15 instructions of
 // overhead per selection (pool refill by lane 0 once per `grab` selections).
-template <int PATH, bool FOLD>
-__device__ __forceinline__ void warp_loop(const SharedParams& P, const TrialStream& ts, uint32_t sbase, float amax,
-                                          Pool pl) {
-  const float amax_s = __fmul_rn(amax, 0x1p-24f);
+template <int PATH>
+__device__ __forceinline__ void warp_loop(const SharedParams& P, const TrialStream& ts, uint32_t sbase, Pool pl) {
   const uint32_t M = P.M;
   const uint32_t half = P.max_trials >> 1;
   const uint32_t calls = half + (P.max_trials & 1u);
@@ -280,8 +273,8 @@ __device__ __forceinline__ void warp_loop(const SharedParams& P, const TrialStre
       const Philox4 x = ts(c, sel);
       const uint32_t j0 = __umulhi(x.x, M);
       const uint32_t j1 = __umulhi(x.z, M);
-      const bool r0 = accept<PATH>(scaled_u<FOLD>(x.y, amax, amax_s), j0, sbase, P.alpha, P.group_shift);
-      const bool r1 = accept<PATH>(scaled_u<FOLD>(x.w, amax, amax_s), j1, sbase, P.alpha, P.group_shift);
+      const bool r0 = accept<PATH>(x.y, j0, sbase, P.thr, P.group_shift);
+      const bool r1 = accept<PATH>(x.w, j1, sbase, P.thr, P.group_shift);
       const bool a0 = (c < calls) & r0;
       const bool a1 = (c < half) & r1;
       const uint32_t b = __ballot_sync(kFull, a0 || a1);
@@ -331,10 +324,10 @@ __global__ void __launch_bounds__(1024, 1) select_shared_kernel(const SharedPara
   __shared__ uint32_t s_g;
   // the next launch's ticket set (its previous user, launch n - 1, has completed)
   if (blockIdx.x == 0 && threadIdx.x < kStripes) P.ctr->next[P.phase ^ 1u][threadIdx.x] = 0ull;
-  // ---- stage the vector (path 1) or its prefilter (paths 2, 3) in smem with one bulk async
+  // ---- stage the thresholds (path 1) or their prefilter (paths 2, 3) in smem with one bulk async
   // copy per CTA (16-byte hull; the data starts `sbase` bytes into it), issued first so that
   // it overlaps the statistics load and the tau phase
-  const uint32_t sbase = (PATH == kPathSmemF32) ? stage_issue(smem, P.alpha, 4u * P.M, &stage_bar)
+  const uint32_t sbase = (PATH == kPathSmemF32) ? stage_issue(smem, P.thr, 4u * P.M, &stage_bar)
                                                 : stage_issue(smem, P.prefilter, 2u * P.n_pref, &stage_bar);
   const DevStats st = *P.stats;
   const uint32_t tid = blockIdx.x * blockDim.x + threadIdx.x;
@@ -360,7 +353,6 @@ __global__ void __launch_bounds__(1024, 1) select_shared_kernel(const SharedPara
   if (invalid || zero) return;  // uniform over the grid; the tickets are untouched
 
   // ---- phase C: trials
-  const float amax = __uint_as_float(st.amax_bits);
   const uint32_t warp_global = tid >> 5;
   const uint32_t g = s_g;
   // static first chunk: half of a warp's fair share; then grabs of ~8192 expected trials
@@ -375,23 +367,12 @@ __global__ void __launch_bounds__(1024, 1) select_shared_kernel(const SharedPara
   Pool pl;
   pool_init(pl, K, nwarps, warp_global, first, grab, P.ctr->next[P.phase], P.no_prefetch == 0u);
   const TrialStream ts(P.seed_lo, P.seed_hi, P.epoch);
-  const bool fold = can_fold(st.amax_bits);
-  if (g == 1u) {
-    if (fold)
-      lane_loop<PATH, true>(P, ts, sbase, amax, pl);
-    else
-      lane_loop<PATH, false>(P, ts, sbase, amax, pl);
-  } else if (g == 32u) {
-    if (fold)
-      warp_loop<PATH, true>(P, ts, sbase, amax, pl);
-    else
-      warp_loop<PATH, false>(P, ts, sbase, amax, pl);
-  } else {
-    if (fold)
-      trial_loop<PATH, true>(P, ts, sbase, amax, g, pl);
-    else
-      trial_loop<PATH, false>(P, ts, sbase, amax, g, pl);
-  }
+  if (g == 1u)
+    lane_loop<PATH>(P, ts, sbase, pl);
+  else if (g == 32u)
+    warp_loop<PATH>(P, ts, sbase, pl);
+  else
+    trial_loop<PATH>(P, ts, sbase, g, pl);
 }
 
 template <int PATH>

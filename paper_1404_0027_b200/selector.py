@@ -12,7 +12,7 @@ import torch
 from . import _abi
 from ._abi import check
 
-PATHS = {0: "none", 1: "smem_f32", 2: "smem_bf16_bracket", 3: "smem_group_max", 4: "rows"}
+PATHS = {0: "none", 1: "smem_thresholds", 2: "smem_bracket16", 3: "smem_group_max", 4: "rows"}
 
 
 def _ptr(t: torch.Tensor | None):

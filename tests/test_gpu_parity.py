@@ -77,7 +77,7 @@ def test_golden_file_values_on_gpu():
 
 def test_c2_yeast_like_full():
     sel, out, ref = _shared_case(synth.yeast_like(), 65536)
-    assert sel.path == "smem_f32"
+    assert sel.path == "smem_thresholds"
     _check(out, ref)
     _, a0, _ = sel.stats()
     assert abs(a0 - ref["a0"][0]) <= 1e-12 * a0
@@ -89,7 +89,7 @@ def test_c3_distributions(kind, M):
     a = synth.distribution(kind, M)
     K = 1 << 14 if not (kind == "pareto" and M == 100_000) else 1 << 12
     sel, out, ref = _shared_case(a, K)
-    assert sel.path == ("smem_f32" if M <= 50_000 else "smem_bf16_bracket")
+    assert sel.path == ("smem_thresholds" if M <= 50_000 else "smem_bracket16")
     _check(out, ref)
     # acceptance rate vs a0/(M amax) within 4 sigma (north_star invariant)
     p = oracle.acceptance_rate(a)
@@ -120,7 +120,7 @@ def test_bf16_bracket_boundaries():
     a = base.view(np.float32).copy()
     a[::11] = 0.0
     sel, out, ref = _shared_case(a, 30_000)
-    assert sel.path == "smem_bf16_bracket"
+    assert sel.path == "smem_bracket16"
     _check(out, ref)
 
 
@@ -175,6 +175,25 @@ def test_epochs_offsets_and_replay():
         assert torch.equal(torch.cat([x, y]), w)
     sel.sync()
     _check(second, oracle.ar_select(a, 5000, seed=SEED, epoch=1, nthreads=8))
+
+
+@pytest.mark.parametrize("scale_exp", [-110, -125, 60])
+def test_extreme_scales_thresholds(scale_exp):
+    # alpha_max below 2^-102 (products of u and alpha_max underflow into subnormals) and
+    # large (2^60: tau stays a normal binary32): the integer acceptance thresholds must reproduce
+    # the oracle's fl32(u * alpha_max) < alpha_j decisions bit for bit
+    a = (synth.yeast_like() * np.float32(2.0 ** scale_exp)).astype(np.float32)
+    assert np.isfinite(a).all() and a.max() > 0
+    _, out, ref = _shared_case(a, 20_000)
+    _check(out, ref)
+
+
+def test_thresholds_on_bf16_and_grid_values():
+    # exact powers of two, values one ulp apart and alpha_j == alpha_max on path 1
+    a = np.array([1.0, np.nextafter(np.float32(1.0), np.float32(0)), 0.5, 0.25 + 2 ** -25, 2 ** -24, 2 ** -25,
+                  0.0, 1.0, 0.75, np.float32(1) - np.float32(2 ** -24)], dtype=np.float32)
+    _, out, ref = _shared_case(a, 50_000)
+    _check(out, ref)
 
 
 def test_power_of_two_scaling_gpu():
