@@ -98,93 +98,94 @@ __global__ void __launch_bounds__(MAXW * 32, 1) select_rows_kernel(const RowsPar
   const uint32_t SB = P.stage_bytes;
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem) + warp * S;
   unsigned char* ring = smem + ((warps * S * 8u + 127u) & ~127u) + (size_t)warp * S * SB;
+  // shared-window addresses, computed once (no generic->shared conversion per row)
+  const uint32_t bars_s = smem_u32(bars);
+  const uint32_t ring_s = smem_u32(ring);
 
   if (lane < S) mbar_init(&bars[lane], 1u);
   asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   __syncwarp();
 
   const uint64_t policy = policy_evict_first();
-  const uint64_t G = gridDim.x;
-  const uint64_t K = P.K;
+  const uint32_t K = P.K;
   const uint32_t M = P.M;
-  const uint64_t row_bytes = P.ld * 4ull;
-  // Row handled by this warp at its n-th step: warps take turns on blocks of B = 2^lb
-  // consecutive rows (block (n/B)*WT + wg), so the rows in flight over the whole GPU stay
-  // within a window of B*WT rows (B = 4: ~58 MB, inside the 256 MB TLB reach) while a warp's
-  // outputs for a block go out as one store per output array from B lanes.
-  const uint64_t WT = G * warps;
-  const uint64_t wg = (uint64_t)blockIdx.x * warps + warp;
+  const uint32_t row_bytes = (uint32_t)(P.ld * 4ull);
+  const unsigned char* base = reinterpret_cast<const unsigned char*>(P.alpha);
+  // Rows of this warp: warps take turns on blocks of B = 2^lb consecutive rows (block
+  // b = wg, wg + WT, ...), so the rows in flight over the whole GPU stay within a window of
+  // B*WT rows (B = 4: ~58 MB, inside the 256 MB TLB reach) while a warp's outputs for a
+  // block go out as one store per output array from B lanes.  The warp's row count is fixed
+  // up front, so the walk below never compares row indices against K.
+  const uint32_t WT = gridDim.x * warps;
+  const uint32_t wg = blockIdx.x * warps + warp;
   const uint32_t lb = P.log2_block;
   const uint32_t bm = (1u << lb) - 1u;
-  auto row_of = [&](uint32_t n) -> uint64_t { return ((((uint64_t)(n >> lb)) * WT + wg) << lb) + (n & bm); };
-  // Incremental walk over this warp's rows (row index, byte offset, position in block): the
-  // per-row bookkeeping is two 64-bit adds instead of 64-bit products.
-  const uint64_t jump = (WT - 1u) * (bm + 1u) + 1u;  // from the last row of a block to the next block
-  const uint64_t jump_bytes = jump * row_bytes;
+  const uint32_t nfull = K >> lb, rem = K & bm;  // full blocks, rows of the partial block
+  const uint32_t n_rows = ((nfull > wg) ? ((nfull - wg - 1u) / WT + 1u) << lb : 0u) +
+                          ((rem != 0u && nfull % WT == wg) ? rem : 0u);
+  auto row_of = [&](uint32_t n) -> uint32_t { return (((n >> lb) * WT + wg) << lb) + (n & bm); };
+  // Incremental walk (row index, position in its block): a few 32-bit ops per row; the byte
+  // offset is one wide multiply.
+  const uint32_t jump = (WT - 1u) * (bm + 1u) + 1u;  // from the last row of a block to the next block
   struct Walk {
-    uint64_t r, off;
-    uint32_t pos;
+    uint32_t r, pos;
   };
   auto advance = [&](Walk& w) {
-    if (w.pos == bm) {
-      w.r += jump;
-      w.off += jump_bytes;
-      w.pos = 0;
-    } else {
-      w.r += 1u;
-      w.off += row_bytes;
-      w.pos += 1u;
-    }
+    const bool last = w.pos == bm;
+    w.r += last ? jump : 1u;
+    w.pos = last ? 0u : w.pos + 1u;
   };
-  auto issue = [&](uint64_t off, uint32_t slot) {
+  auto issue = [&](uint32_t r, uint32_t slot) {
+    const uint64_t off = (uint64_t)r * row_bytes;
     const uint64_t a = off & ~15ull;
     const uint64_t e = (off + 4ull * M + 15ull) & ~15ull;
     const uint32_t bytes = (uint32_t)(e - a);
-    mbar_arrive_expect_tx(&bars[slot], bytes);
-    bulk_g2s(ring + (size_t)slot * SB, reinterpret_cast<const unsigned char*>(P.alpha) + a, bytes, &bars[slot],
-             policy);
+    mbar_arrive_expect_tx_s(bars_s + 8u * slot, bytes);
+    bulk_g2s_s(ring_s + slot * SB, base + a, bytes, bars_s + 8u * slot, policy);
   };
-  Walk cur{wg << lb, (wg << lb) * row_bytes, 0u};
+  Walk cur{wg << lb, 0u};
   Walk pre = cur;  // row n + S: the next row to prefetch into the slot row n frees
   for (uint32_t i = 0; i < S; ++i) {
-    if (lane == 0 && pre.r < K) issue(pre.off, i);
+    if (lane == 0 && i < n_rows) issue(pre.r, i);
     advance(pre);
   }
 
   const uint32_t half = P.max_trials >> 1;
   const uint32_t calls = half + (P.max_trials & 1u);
   const TrialStream ts(P.seed_lo, P.seed_hi, P.epoch);
-  float nlog = 0.f;                     // -ln(u1) of row_of(n0 + lane)
-  // this lane's buffered outputs for row (block base + lane)
+  float nlog = 0.f;  // -ln(u1) of row_of(n0 + lane)
+  // this lane's buffered outputs for row (block base + lane); tau is formed at the flush,
+  // one division per block: tau = -ln(u1) / fl32(alpha_0), with fl32(alpha_0) = 0 for an
+  // all-zero row (tau = +inf) and NaN for an invalid one (tau = NaN)
   int32_t o_id = -1;
   uint32_t o_tr = 0;
-  float o_tau = 0.f;
+  float o_a0f = 0.f;
   double o_a0 = 0.0;
 
-  for (uint32_t n = 0; cur.r < K; ++n) {
-    const uint64_t r = cur.r;
+  for (uint32_t n = 0; n < n_rows; ++n) {
+    const uint32_t r = cur.r;
     const uint32_t slot = n & (S - 1u);
     const uint32_t parity = (n >> lS) & 1u;
     if ((n & 31u) == 0u && MODE != kModeStats) {
-      const uint64_t rr = row_of(n + lane);
-      nlog = rr < K ? neg_log_u1(P.seed_lo, P.seed_hi, P.s0 + (uint32_t)rr, P.epoch) : 0.f;
+      const uint32_t nn = n + lane;
+      nlog = nn < n_rows ? neg_log_u1(P.seed_lo, P.seed_hi, P.s0 + row_of(nn), P.epoch) : 0.f;
     }
-    mbar_wait(&bars[slot], parity);
+    mbar_wait_s(bars_s + 8u * slot, parity);
     // The slot holds the row's 16-byte hull: element j sits at word lead + j.
-    const uint32_t lead = (uint32_t)(cur.off & 15ull) >> 2;
-    const uint32_t row_s = smem_u32(ring + (size_t)slot * SB) + 4u * lead;
+    const uint32_t lead = (r * row_bytes & 15u) >> 2;
+    const uint32_t row_s = ring_s + slot * SB + 4u * lead;
 
     // ---- alpha_max (max of bit patterns) and alpha_0.  Each lane takes 16 elements per
     // 512-chunk (conflict-free scalar LDS, consecutive lanes), sums them pairwise in binary32
     // (depth 4, packed FADD2) and adds the chunk sum in binary64; a last 256-chunk likewise
-    // with 8, the < 256 tail sequentially (<= 8 per lane).  Relative error of alpha_0 before
-    // the final rounding <= 7u (R11).  (A 16-byte-vector variant measured slower:
-    // profiles/r01_c4_select_rows_v3.md.)
+    // with 8, the < 256 tail in warp-wide steps of 32 (<= 8 per lane, sequential).  Relative
+    // error of alpha_0 before the final rounding <= 7u (R11).  (A 16-byte-vector
+    // variant measured slower: profiles/r01_c4_select_rows_v3.md.)
     uint32_t mx = 0;
     double acc = 0.0;
-    uint32_t base = 0;
-    for (; base + 512u <= M; base += 512u) {
-      const uint32_t p = row_s + 4u * (base + lane);
+    uint32_t b0 = 0;
+    for (; b0 + 512u <= M; b0 += 512u) {
+      const uint32_t p = row_s + 4u * (b0 + lane);
       float v[16];
 #pragma unroll
       for (int k = 0; k < 16; ++k) {
@@ -194,31 +195,32 @@ __global__ void __launch_bounds__(MAXW * 32, 1) select_rows_kernel(const RowsPar
       float2 q[8];
 #pragma unroll
       for (int k = 0; k < 8; ++k) q[k] = make_float2(v[2 * k], v[2 * k + 1]);
-      const float2 r = fadd2_rn(fadd2_rn(fadd2_rn(q[0], q[1]), fadd2_rn(q[2], q[3])),
-                                fadd2_rn(fadd2_rn(q[4], q[5]), fadd2_rn(q[6], q[7])));
-      acc += (double)__fadd_rn(r.x, r.y);
+      const float2 rr = fadd2_rn(fadd2_rn(fadd2_rn(q[0], q[1]), fadd2_rn(q[2], q[3])),
+                                 fadd2_rn(fadd2_rn(q[4], q[5]), fadd2_rn(q[6], q[7])));
+      acc += (double)__fadd_rn(rr.x, rr.y);
     }
-    if (base + 256u <= M) {
-      const uint32_t p = row_s + 4u * (base + lane);
+    if (b0 + 256u <= M) {
+      const uint32_t p = row_s + 4u * (b0 + lane);
       float v[8];
 #pragma unroll
       for (int k = 0; k < 8; ++k) {
         v[k] = lds_f32(p + 128u * k);
         mx = max(mx, __float_as_uint(v[k]));
       }
-      const float2 r = fadd2_rn(fadd2_rn(make_float2(v[0], v[1]), make_float2(v[2], v[3])),
-                                fadd2_rn(make_float2(v[4], v[5]), make_float2(v[6], v[7])));
-      acc += (double)__fadd_rn(r.x, r.y);
-      base += 256u;
+      const float2 rr = fadd2_rn(fadd2_rn(make_float2(v[0], v[1]), make_float2(v[2], v[3])),
+                                 fadd2_rn(make_float2(v[4], v[5]), make_float2(v[6], v[7])));
+      acc += (double)__fadd_rn(rr.x, rr.y);
+      b0 += 256u;
     }
-    {
-      float s = 0.f;  // tail: < 256 elements, at most 8 per lane, sequential
-      for (uint32_t j = base + lane; j < M; j += 32u) {
-        const float v = lds_f32(row_s + 4u * j);
+    if (b0 < M) {  // tail: warp-uniform trip count, one predicated load per lane per step
+      float sum = 0.f;
+#pragma unroll 1
+      for (uint32_t j = b0; j < M; j += 32u) {
+        const float v = (j + lane < M) ? lds_f32(row_s + 4u * (j + lane)) : 0.f;
         mx = max(mx, __float_as_uint(v));
-        s = __fadd_rn(s, v);
+        sum = __fadd_rn(sum, v);  // + 0.0 leaves a sum of non-negative values unchanged
       }
-      acc += (double)s;
+      acc += (double)sum;
     }
     mx = __reduce_max_sync(kFull, mx);
 #pragma unroll
@@ -227,23 +229,22 @@ __global__ void __launch_bounds__(MAXW * 32, 1) select_rows_kernel(const RowsPar
     const uint32_t nl32 = cur.pos;  // this row's slot in the block's output buffer
     if constexpr (MODE == kModeStats) {
       if (lane == nl32) {
-        o_tau = mx < kInfBits ? __uint_as_float(mx) : __uint_as_float(0x7fc00000u);
+        o_a0f = mx < kInfBits ? __uint_as_float(mx) : __uint_as_float(0x7fc00000u);
         o_a0 = mx < kInfBits ? acc : __longlong_as_double(0x7ff8000000000000ll);
       }
     } else {
-      const float nl = __shfl_sync(kFull, nlog, n & 31u);
       int32_t id = -1;
       uint32_t tr = 0;
-      float tau;
+      float a0f;
       if (mx >= kInfBits) {  // invalid row: sticky EPROPENSITY
-        tau = __uint_as_float(0x7fc00000u);
+        a0f = __uint_as_float(0x7fc00000u);
         if (lane == 0) atomicOr(&P.ctr->err, 1u);
       } else if (mx == 0u) {  // all-zero row: nothing can fire
-        tau = __uint_as_float(kInfBits);
+        a0f = 0.f;
       } else {
         const float amax = __uint_as_float(mx);
-        tau = __fdiv_rn(nl, __double2float_rn(acc));
-        const uint32_t sel = ts.sel_word(P.s0 + (uint32_t)r);
+        a0f = __double2float_rn(acc);
+        const uint32_t sel = ts.sel_word(P.s0 + r);
         if constexpr (MODE == kRuleArgmin) {
           // the paper's printed rule on this row: election + argmin selection
           const float T = __fmul_rn(P.w, amax);
@@ -264,27 +265,32 @@ __global__ void __launch_bounds__(MAXW * 32, 1) select_rows_kernel(const RowsPar
       }
       if (lane == nl32) {
         o_id = id;
-        o_tau = tau;
+        o_a0f = a0f;
         o_tr = tr;
       }
     }
-    if (nl32 == bm || r + 1u >= K) {  // flush the block: one coalesced store per output
-      const uint64_t rl = r - nl32 + lane;
-      if (lane <= nl32) {
-        if constexpr (MODE == kModeStats) {
-          P.amax_out[rl] = o_tau;
+    if (nl32 == bm || n + 1u == n_rows) {  // flush the block: one coalesced store per output
+      const uint32_t rl = r - nl32 + lane;
+      if constexpr (MODE == kModeStats) {
+        if (lane <= nl32) {
+          P.amax_out[rl] = o_a0f;
           P.a0_out[rl] = o_a0;
-        } else {
+        }
+      } else {
+        // -ln(u1) of this lane's row sits in lane (n - nl32 + lane) & 31 of the batch (a
+        // block never straddles a batch: 32 is a multiple of B)
+        const float nl = __shfl_sync(kFull, nlog, (n - nl32 + lane) & 31u);
+        if (lane <= nl32) {
           P.idx[rl] = o_id;
-          if (P.tau) P.tau[rl] = o_tau;
+          if (P.tau) P.tau[rl] = __fdiv_rn(nl, o_a0f);
           if (P.trials) P.trials[rl] = o_tr;
         }
       }
     }
     __syncwarp();
-    if (lane == 0 && pre.r < K) {
+    if (lane == 0 && n + S < n_rows) {
       fence_proxy_async_smem();  // generic-proxy reads of the slot precede the async refill
-      issue(pre.off, slot);
+      issue(pre.r, slot);
     }
     advance(cur);
     advance(pre);
