@@ -280,6 +280,65 @@ __device__ __forceinline__ uint32_t lanemask_lt() {
   return m;
 }
 
+// ---------------------------------------------------------------- row reduction
+// alpha_max (max of bit patterns: exact, and >= 0x7f800000 flags an invalid value) and
+// alpha_0 of one M-element row in shared memory at `row_s`, by one warp, in a FIXED order
+// (R11), shared by the matrix kernel and the SSA kernel so that an SSA step and
+// gpuar_select on the same row see the same bits.  Each lane takes 16 elements per
+// 512-chunk (conflict-free scalar LDS, consecutive lanes), sums them pairwise in binary32
+// (depth 4, packed FADD2) and adds the chunk sum in binary64; a last 256-chunk likewise with
+// 8; the < 256 tail in warp-wide steps of 32 (<= 8 per lane, sequential); then a 5-level
+// xor butterfly in binary64.  Relative error of alpha_0 <= 8u before the final rounding.
+// (A 16-byte-vector variant measured slower: profiles/r01_c4_select_rows_v3.md.)
+__device__ __forceinline__ void row_reduce(uint32_t row_s, uint32_t M, uint32_t lane, uint32_t& mx_out,
+                                           double& acc_out) {
+  uint32_t mx = 0;
+  double acc = 0.0;
+  uint32_t b0 = 0;
+  for (; b0 + 512u <= M; b0 += 512u) {
+    const uint32_t p = row_s + 4u * (b0 + lane);
+    float v[16];
+#pragma unroll
+    for (int k = 0; k < 16; ++k) {
+      v[k] = lds_f32(p + 128u * k);
+      mx = max(mx, __float_as_uint(v[k]));
+    }
+    float2 q[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) q[k] = make_float2(v[2 * k], v[2 * k + 1]);
+    const float2 rr = fadd2_rn(fadd2_rn(fadd2_rn(q[0], q[1]), fadd2_rn(q[2], q[3])),
+                               fadd2_rn(fadd2_rn(q[4], q[5]), fadd2_rn(q[6], q[7])));
+    acc += (double)__fadd_rn(rr.x, rr.y);
+  }
+  if (b0 + 256u <= M) {
+    const uint32_t p = row_s + 4u * (b0 + lane);
+    float v[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      v[k] = lds_f32(p + 128u * k);
+      mx = max(mx, __float_as_uint(v[k]));
+    }
+    const float2 rr = fadd2_rn(fadd2_rn(make_float2(v[0], v[1]), make_float2(v[2], v[3])),
+                               fadd2_rn(make_float2(v[4], v[5]), make_float2(v[6], v[7])));
+    acc += (double)__fadd_rn(rr.x, rr.y);
+    b0 += 256u;
+  }
+  if (b0 < M) {  // tail: warp-uniform trip count, one predicated load per lane per step
+    float sum = 0.f;
+#pragma unroll 1
+    for (uint32_t j = b0; j < M; j += 32u) {
+      const float v = (j + lane < M) ? lds_f32(row_s + 4u * (j + lane)) : 0.f;
+      mx = max(mx, __float_as_uint(v));
+      sum = __fadd_rn(sum, v);  // + 0.0 leaves a sum of non-negative values unchanged
+    }
+    acc += (double)sum;
+  }
+  mx_out = __reduce_max_sync(kFull, mx);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(kFull, acc, o);
+  acc_out = acc;
+}
+
 // ---------------------------------------------------------------- launchers (host)
 
 cudaError_t launch_stats(const float* alpha, uint32_t M, double* part_sum, uint32_t* part_max,

@@ -6,8 +6,8 @@
 // One warp owns one realization at a time; its state X (N int32) and its propensity row
 // (M binary32) live in the warp's shared-memory slice, the reaction network (reactants,
 // rate constants, sparse change vectors) is staged once per CTA.  Per step: mass-action
-// propensities (R20) written to the row while reducing alpha_max / alpha_0
-// exactly as the matrix kernel does, tau, the first-accept trials of kernels_rows.cu,
+// propensities (R20) in the row, alpha_max / alpha_0 by row_reduce (the matrix
+// kernel's code and order), tau, the first-accept trials of kernels_rows.cu,
 // then X += v_j and t += tau -- nothing leaves the SM until the run ends.  Realization
 // k is selection s0 + k and step i uses epoch epoch0 + i, so every step is bit-identical
 // to a gpuar_select on the same row.
@@ -94,7 +94,6 @@ __global__ void __launch_bounds__(768, 1) ssa_kernel(const SsaParams P) {
   const uint32_t calls = half + (P.max_trials & 1u);
   TrialStream ts(P.seed_lo, P.seed_hi, P.epoch0);
   const uint32_t WT = gridDim.x * warps;
-  const uint32_t full_chunks = M >> 8;
 
   for (uint32_t k = blockIdx.x * warps + warp; k < P.K; k += WT) {
     int32_t* Xg = P.X + (size_t)k * N;
@@ -107,46 +106,16 @@ __global__ void __launch_bounds__(768, 1) ssa_kernel(const SsaParams P) {
     float nlog = 0.f;  // -ln(u1) of step (step & ~31) + lane: tau draws 32 steps at a time
     for (int32_t step = 0; step < P.n_steps; ++step) {
       if ((step & 31) == 0) nlog = neg_log_u1(P.seed_lo, P.seed_hi, s, P.epoch0 + (uint32_t)(step + (int32_t)lane));
-      // ---- propensities -> row (all of them on the first step of the call, else only the
-      // dependents of the last fired reaction, already updated below), with alpha_max (bits)
-      // and alpha_0 reduced over the whole row in a fixed order (as in kernels_rows.cu)
-      const bool full = step == 0 || !deps;
-      uint32_t mx = 0;
-      double acc = 0.0;
-      for (uint32_t ch = 0; ch < full_chunks; ++ch) {
-        float v[8];
-#pragma unroll
-        for (int q = 0; q < 8; ++q) {
-          const uint32_t j = ch * 256u + (uint32_t)q * 32u + lane;
-          if (full) {
-            v[q] = propensity(xs, lds_i4(desc_s + 16u * j));
-            row[j] = v[q];
-          } else {
-            v[q] = lds_f32(row_s + 4u * j);
-          }
-          mx = max(mx, __float_as_uint(v[q]));
-        }
-        acc += (double)__fadd_rn(__fadd_rn(__fadd_rn(v[0], v[1]), __fadd_rn(v[2], v[3])),
-                                 __fadd_rn(__fadd_rn(v[4], v[5]), __fadd_rn(v[6], v[7])));
+      // ---- propensities -> row: all of them on the first step of the call (else only the
+      // dependents of the last fired reaction, already updated below), then alpha_max (bits)
+      // and alpha_0 over the whole row in the fixed order of the matrix kernel (row_reduce)
+      if (step == 0 || !deps) {
+        for (uint32_t j = lane; j < M; j += 32u) row[j] = propensity(xs, lds_i4(desc_s + 16u * j));
+        __syncwarp();
       }
-      {
-        float sum = 0.f;
-        for (uint32_t j = (full_chunks << 8) + lane; j < M; j += 32u) {
-          float v;
-          if (full) {
-            v = propensity(xs, lds_i4(desc_s + 16u * j));
-            row[j] = v;
-          } else {
-            v = lds_f32(row_s + 4u * j);
-          }
-          mx = max(mx, __float_as_uint(v));
-          sum = __fadd_rn(sum, v);
-        }
-        acc += (double)sum;
-      }
-      mx = __reduce_max_sync(kFull, mx);
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(kFull, acc, o);
+      uint32_t mx;
+      double acc;
+      row_reduce(row_s, M, lane, mx, acc);
       __syncwarp();  // row complete before the gathers
       if (mx >= kInfBits) {  // invalid propensity: sticky EPROPENSITY, stop this realization
         if (lane == 0) atomicOr(&P.ctr->err, 1u);

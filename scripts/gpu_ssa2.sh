@@ -1,0 +1,16 @@
+#!/bin/bash
+mkdir -p gpurun_out/ssa2
+timeout 900 python -m pytest tests/test_gpu_ssa.py tests/test_gpu_parity.py -m gpu -x -q -k "ssa or rows or c4 or yeast or dimer or immigration or chunk" > gpurun_out/ssa2/tests.log 2>&1
+tail -3 gpurun_out/ssa2/tests.log
+timeout 600 python bench.py --config s1 --steps 20 --no-cpu > gpurun_out/ssa2/s1.json 2>&1
+python -c "
+import json; l=[x for x in open('gpurun_out/ssa2/s1.json') if x.startswith('{')]
+r=json.loads(l[-1]) if l else None
+print('s1', '%.4g'%r['value'] if r else open('gpurun_out/ssa2/s1.json').read()[-300:], r and r['ms_per_step'], r and r['clocks'])"
+timeout 300 python bench.py --steps 300 --no-cpu --no-e2e > gpurun_out/ssa2/c4.json 2>&1
+python -c "
+import json; l=[x for x in open('gpurun_out/ssa2/c4.json') if x.startswith('{')]
+r=json.loads(l[-1]) if l else None
+print('c4', '%.4g'%r['value'] if r else open('gpurun_out/ssa2/c4.json').read()[-300:], r and r['ms_per_step'], r and r['clocks'])"
+timeout 600 ncu --set full --clock-control none --import-source on -k regex:ssa_kernel -s 1 -c 1 -o gpurun_out/prof_s1_v22 python bench.py --config s1 --steps 1 --warmup 3 --no-cpu --no-e2e > gpurun_out/ssa2/ncu.log 2>&1
+tail -1 gpurun_out/ssa2/ncu.log
