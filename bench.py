@@ -426,10 +426,45 @@ def run_gpuar(args, w, rank, world, local_rank):
         for _ in range(args.e2e_steps):
             sel.select_host(host, K=K, out=hout)
         dt = time.perf_counter() - t0
-        e2e = {"value": K * world * args.e2e_steps / max_over_ranks(dt, device), "unit": UNIT,
+        dt_max = max_over_ranks(dt, device)
+        e2e = {"value": K * world * args.e2e_steps / dt_max, "unit": UNIT,
                "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": 12 * K, "steps": args.e2e_steps,
+               # the bound of this number: host<->device bytes per second through PCIe
+               "pcie_gbs": (h2d + 12 * K) * args.e2e_steps / dt_max / 1e9,
                "timer": "host wall clock around synchronous gpuar_select_host, max over ranks"}
         del host
+
+    # Short calls: the same selections replayed from a CUDA graph of
+    # consecutive gpuar_select launches (an even number: alternate launches use alternate
+    # ticket sets) -- device throughput without the per-call host launch cost.  Secondary
+    # figure; `value` above is the plain per-call loop.
+    graph = None
+    if w["kind"] == "shared" and ms_step < 0.1 and world == 1:
+        try:
+            n_calls = 100
+            gs = torch.cuda.Stream(device)
+            gs.wait_stream(stream)
+            with torch.cuda.stream(gs):
+                sel.select(K, out=out)             # moves the handle to gs outside the capture
+                gs.synchronize()
+                cg = torch.cuda.CUDAGraph()
+                with torch.cuda.graph(cg, stream=gs):
+                    for _ in range(n_calls):
+                        sel.select(K, out=out)
+                cg.replay()
+                g0, g1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                reps = 20
+                g0.record(gs)
+                for _ in range(reps):
+                    cg.replay()
+                g1.record(gs)
+                g1.synchronize()
+            gms = g0.elapsed_time(g1) / (reps * n_calls)
+            graph = {"value": K / (gms * 1e-3), "unit": UNIT, "us_per_call": gms * 1e3, "calls_per_graph": n_calls,
+                     "note": "CUDA-graph replay of consecutive selects (same epochs each replay)"}
+            sel._stream()                          # back to the default stream for what follows
+        except Exception as exc:                   # informational only
+            graph = {"error": str(exc)[:200]}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
@@ -455,6 +490,7 @@ def run_gpuar(args, w, rank, world, local_rank):
             "e2e": e2e,
             "gpu_launches": args.steps,
             "clocks": clocks,
+            "graph_steady_state": graph,
             "validation": {"trials_sum_last_step": trials_sum, "rejected_last_step": rejected,
                            "mean_trials": trials_sum / (K * world)},
         }
