@@ -15,3 +15,5 @@ timeout 300 python bench.py --config c4 --rule argmin --steps 20 --no-e2e > gpur
 timeout 300 python bench.py --config c2 --rule it --steps 300 --no-e2e > gpurun_out/final/c2_it.json 2>&1
 timeout 600 python bench.py --config s1 --steps 20 > gpurun_out/final/s1.json 2>&1
 timeout 120 python scripts/philox_peak.py > gpurun_out/final/philox_peak.txt 2>&1
+timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/final/launches_c4_final.csv python bench.py --steps 5 --warmup 3 --no-e2e --no-cpu > gpurun_out/final/launches_c4.log 2>&1
+python scripts/collect_results.py gpurun_out/final > gpurun_out/final/results.md
