@@ -196,6 +196,28 @@ def test_thresholds_on_bf16_and_grid_values():
     _check(out, ref)
 
 
+def test_top_of_selection_and_epoch_range():
+    # selection indices up to 2^32 - 1 and the largest epoch: counter words 1 and 2 at their
+    # maxima, on the shared-vector and the matrix paths
+    K = 5000
+    s0 = (1 << 32) - K
+    a = synth.yeast_like()
+    _, out, ref = _shared_case(a, K, epoch=0xFFFFFFFF, s0=s0)
+    _check(out, ref)
+    _, out, ref, _ = _rows_case(1029, K, k0=s0, epoch=0xFFFFFFFF)
+    _check(out, ref)
+
+
+@pytest.mark.slow
+def test_huge_shared_vector_group_path():
+    # M = 2^26 (268 MB vector): 1024-reaction groups in the shared-memory prefilter
+    M = 1 << 26
+    a = synth.uniform(M)
+    sel, out, ref = _shared_case(a, 4096)
+    assert sel.path == "smem_group_max"
+    _check(out, ref)
+
+
 def test_power_of_two_scaling_gpu():
     a = synth.yeast_like()
     _, base, _ = _shared_case(a, 20_000)
