@@ -378,6 +378,18 @@ def run_gpuar(args, w, rank, world, local_rank):
     else:
         calls = int(((out[2].to(torch.int64) + 1) // 2).sum().item()) + K   # Philox calls of the last launch
 
+    # useful-trial fraction = sum(trials) / trials computed; a team of g lanes
+    # computes whole rounds of 2g canonical trials (g = 32 on the matrix path)
+    trials_info = None
+    if w["rule"] == "classic":
+        g = 32 if w["kind"] == "rows" else sel.last_team
+        if g > 0:
+            t = out[2].to(torch.int64)
+            computed = int((((t + 2 * g - 1) // (2 * g)) * (2 * g)).sum().item())
+            useful = int(t.sum().item())
+            trials_info = {"team": g, "trials_useful": useful, "trials_computed": computed,
+                           "useful_trial_fraction": useful / computed if computed else None}
+
     peaks = measured_peaks()
     clocks = clk.summary()
     if w["kind"] == "rows":
@@ -493,6 +505,7 @@ def run_gpuar(args, w, rank, world, local_rank):
             "graph_steady_state": graph,
             "validation": {"trials_sum_last_step": trials_sum, "rejected_last_step": rejected,
                            "mean_trials": trials_sum / (K * world)},
+            "trials": trials_info,
         }
         if w["rule"] == "argmin":
             # the paper's Table 1 metric on the last step's histogram and

@@ -201,6 +201,14 @@ int gpuar_bench_philox(gpuar_t h, int64_t n_threads, int32_t calls, uint32_t *d_
  * memory, 4 per-realization rows).  Pure host query. */
 int gpuar_path(gpuar_t h, int32_t *path);
 
+/* Team size (lanes per selection, a power of two in [1, 32]) the last classic-rule
+ * gpuar_select on a shared vector used, as chosen on the device from p and K (DESIGN.md
+ * §5.2); a round of a team covers 2*team consecutive canonical trials, so the trials a
+ * selection computed are 2*team*ceil(trials/(2*team)).  0 before any such select.  The
+ * matrix path always uses whole warps (32).  Synchronous (drains the handle's stream).
+ * Errors: EINVAL, ECUDA. */
+int gpuar_last_team(gpuar_t h, int32_t *team);
+
 /* Static text for a status code. */
 const char *gpuar_strerror(int status);
 

@@ -43,6 +43,7 @@ SIGNATURES = {
     "gpuar_histogram": (_int, [_vp, _vp, _vp, _i64, _vp, _vp]),
     "gpuar_bench_philox": (_int, [_vp, _i64, _i32, _vp]),
     "gpuar_path": (_int, [_vp, ctypes.POINTER(_i32)]),
+    "gpuar_last_team": (_int, [_vp, ctypes.POINTER(_i32)]),
     "gpuar_strerror": (ctypes.c_char_p, [_int]),
 }
 

@@ -756,6 +756,18 @@ int gpuar_bench_philox(gpuar_t h, int64_t n_threads, int32_t calls, uint32_t* d_
                                          (uint32_t)(h->seed >> 32), d_sink, h->stream));
 }
 
+int gpuar_last_team(gpuar_t h, int32_t* team) {
+  if (!h || !team) return GPUAR_EINVAL;
+  DeviceGuard g(h->device);
+  if (!g.ok) return GPUAR_ECUDA;
+  unsigned int t = 0;
+  cudaError_t e = cudaMemcpyAsync(&t, &h->d_ctr->team, sizeof(t), cudaMemcpyDeviceToHost, h->stream);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(h->stream);
+  if (e != cudaSuccess) return cuda_status(e);
+  *team = (int32_t)t;
+  return GPUAR_OK;
+}
+
 int gpuar_path(gpuar_t h, int32_t* path) {
   if (!h || !path) return GPUAR_EINVAL;
   *path = h->path;

@@ -29,6 +29,7 @@ struct DevCounters {
   // completed in stream order) -- no end-of-launch counter or fence.
   unsigned long long next[2][kStripes];
   unsigned int err;                   // sticky EPROPENSITY flag (cleared by the host)
+  unsigned int team;                  // team size of the last shared-vector classic launch
 };
 
 enum Path : int {

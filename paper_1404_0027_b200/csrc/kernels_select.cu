@@ -355,6 +355,7 @@ __global__ void __launch_bounds__(1024, 1) select_shared_kernel(const SharedPara
   // ---- phase C: trials
   const uint32_t warp_global = tid >> 5;
   const uint32_t g = s_g;
+  if (tid == 0) P.ctr->team = g;
   // static first chunk: half of a warp's fair share; then grabs of ~8192 expected trials
   // (st.grab), at most an eighth of the fair share (but two teams' worth), at least one
   // selection per team; tickets are prefetched one chunk ahead.

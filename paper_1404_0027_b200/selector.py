@@ -96,6 +96,13 @@ class Selector:
         check(self._lib.gpuar_set_max_trials(self._h, int(n)), "gpuar_set_max_trials")
 
     @property
+    def last_team(self) -> int:
+        """gpuar_last_team: lanes per selection of the last shared-vector classic select."""
+        g = ctypes.c_int32()
+        check(self._lib.gpuar_last_team(self._h, ctypes.byref(g)), "gpuar_last_team")
+        return int(g.value)
+
+    @property
     def path(self) -> str:
         p = ctypes.c_int32()
         check(self._lib.gpuar_path(self._h, ctypes.byref(p)), "gpuar_path")

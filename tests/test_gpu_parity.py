@@ -218,6 +218,19 @@ def test_huge_shared_vector_group_path():
     _check(out, ref)
 
 
+def test_last_team_reports_the_device_choice():
+    sel = _sel(1029, 65536)
+    assert sel.last_team == 0                       # no shared-vector select yet
+    sel.set_propensities(torch.from_numpy(synth.yeast_like()).cuda())
+    sel.select(65536)
+    g = sel.last_team
+    assert g in (1, 2, 4, 8, 16, 32)
+    sel2 = _sel(1000, 1 << 20)
+    sel2.set_propensities(torch.from_numpy(synth.uniform(1000)).cuda())
+    sel2.select(1 << 20)
+    assert sel2.last_team == 1                      # p ~ 0.5, many selections: one lane each
+
+
 def test_power_of_two_scaling_gpu():
     a = synth.yeast_like()
     _, base, _ = _shared_case(a, 20_000)
