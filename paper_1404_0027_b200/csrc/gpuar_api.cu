@@ -320,7 +320,7 @@ int gpuar_create(gpuar_t* out, int64_t M, int64_t K, uint64_t seed) {
   set_ssa_limits(h->smem_optin);
   set_it_limits(h->smem_optin);
   {
-    const size_t am_sh = (size_t)((M + 3) & ~3ll) * 4u;
+    const size_t am_sh = (size_t)((M + 3) & ~3ll) * 8u;  // alpha and RN(1/alpha) in smem
     h->am_smem = am_sh + 1024u <= (size_t)h->smem_optin;
     h->am_grid = h->num_sms * 8;  // 8 x 256 threads per SM (occupancy-capped by the runtime)
   }

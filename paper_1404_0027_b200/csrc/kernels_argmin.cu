@@ -23,18 +23,32 @@ namespace gpuar {
 
 namespace {
 
+// The rating RN(t / d) with the reaction's correctly rounded reciprocal y = RN(1/d) staged
+// beside it: q0 = RN(t y), r = t - d q0 (exact with an FMA), q = RN(q0 + r y) -- the final
+// correction of IEEE division by Newton-Raphson with an FMA (Markstein), which returns the
+// correctly rounded quotient when nothing underflows or overflows; the caller guarantees
+// that (R23), so this is bit-identical to __fdiv_rn(t, d) at 3 instead of ~8
+// instructions (no MUFU.RCP, no reciprocal refinement, no FCHK slow-path test).
+__device__ __forceinline__ float div_by_recip(float t, float d, float y) {
+  const float q0 = __fmul_rn(t, y);
+  return __fmaf_rn(__fmaf_rn(-q0, d, t), y, q0);
+}
+
 // election: eligible iff t < d (d = 0 is never eligible since t >= 0), rating t / d; a
 // lane sees its reactions in increasing j, so a strict `<` keeps the lowest index on ties.
-__device__ __forceinline__ void elect(float t, float d, uint32_t j, float& bestR, uint32_t& bestJ) {
-  const float R = (t < d) ? __fdiv_rn(t, d) : 1.0f;
+template <bool FASTDIV>
+__device__ __forceinline__ void elect(float t, float d, float y, uint32_t j, float& bestR, uint32_t& bestJ) {
+  float R = 1.0f;
+  if (t < d) R = FASTDIV ? div_by_recip(t, d, y) : __fdiv_rn(t, d);
   if (R < bestR) {
     bestR = R;
     bestJ = j;
   }
 }
 
-template <bool SMEM, bool FOLD>
-__device__ __forceinline__ void argmin_teams(const SharedParams& P, uint32_t sbase, float T, uint32_t g) {
+template <bool SMEM, bool FOLD, bool FASTDIV>
+__device__ __forceinline__ void argmin_teams(const SharedParams& P, uint32_t sbase, uint32_t rbase, float T,
+                                             uint32_t g) {
   const float T_s = __fmul_rn(T, 0x1p-24f);
   const uint32_t M = P.M, K = P.K;
   const uint32_t calls = (M + 3u) >> 2;
@@ -57,19 +71,20 @@ __device__ __forceinline__ void argmin_teams(const SharedParams& P, uint32_t sba
     for (uint32_t c = rank; c < calls; c += g) {
       const Philox4 x = ts(c, sel);
       const uint32_t j = 4u * c;
-      float4 d;
+      float4 d, y = make_float4(0.f, 0.f, 0.f, 0.f);
       if constexpr (SMEM) {
         d = lds_f32x4(sbase + 16u * c);  // zero-padded to a multiple of 4 in smem
+        if constexpr (FASTDIV) y = lds_f32x4(rbase + 16u * c);
       } else {
         d.x = __ldg(P.alpha + j);
         d.y = j + 1u < M ? __ldg(P.alpha + j + 1u) : 0.f;
         d.z = j + 2u < M ? __ldg(P.alpha + j + 2u) : 0.f;
         d.w = j + 3u < M ? __ldg(P.alpha + j + 3u) : 0.f;
       }
-      elect(scaled_u<FOLD>(x.x, T, T_s), d.x, j, bestR, bestJ);
-      elect(scaled_u<FOLD>(x.y, T, T_s), d.y, j + 1u, bestR, bestJ);
-      elect(scaled_u<FOLD>(x.z, T, T_s), d.z, j + 2u, bestR, bestJ);
-      elect(scaled_u<FOLD>(x.w, T, T_s), d.w, j + 3u, bestR, bestJ);
+      elect<FASTDIV>(scaled_u<FOLD>(x.x, T, T_s), d.x, y.x, j, bestR, bestJ);
+      elect<FASTDIV>(scaled_u<FOLD>(x.y, T, T_s), d.y, y.y, j + 1u, bestR, bestJ);
+      elect<FASTDIV>(scaled_u<FOLD>(x.z, T, T_s), d.z, y.z, j + 2u, bestR, bestJ);
+      elect<FASTDIV>(scaled_u<FOLD>(x.w, T, T_s), d.w, y.w, j + 3u, bestR, bestJ);
     }
     // team minimum of the lexicographic (rating bits, index) key
     unsigned long long best = ((unsigned long long)__float_as_uint(bestR) << 32) | bestJ;
@@ -101,27 +116,45 @@ __global__ void __launch_bounds__(256) argmin_shared_kernel(const SharedParams P
     }
   }
   if (invalid || zero) return;
-  if constexpr (SMEM) {  // zero-padded to a multiple of 4 (LDS.128 per Philox call)
+  const uint32_t padded = (P.M + 3u) & ~3u;
+  if constexpr (SMEM) {  // alpha and RN(1/alpha), zero-padded to a multiple of 4 (LDS.128 per call)
     float* sv = reinterpret_cast<float*>(smem);
-    const uint32_t padded = (P.M + 3u) & ~3u;
-    for (uint32_t j = threadIdx.x; j < padded; j += blockDim.x) sv[j] = j < P.M ? __ldg(P.alpha + j) : 0.f;
+    float* sr = sv + padded;
+    for (uint32_t j = threadIdx.x; j < padded; j += blockDim.x) {
+      const float a = j < P.M ? __ldg(P.alpha + j) : 0.f;
+      sv[j] = a;
+      // (a reaction with alpha < 2^-100 is eligible only for t = 0, where q = 0 for y = 0)
+      sr[j] = a >= 0x1p-100f ? __frcp_rn(a) : 0.f;
+    }
     __syncthreads();
   }
   const float T = __fmul_rn(P.w, __uint_as_float(st.amax_bits));
   const uint32_t calls = (P.M + 3u) >> 2;
   uint32_t g = 1u;
   while (g < 32u && g < calls) g <<= 1;  // one or a few calls per lane
-  if (can_fold(__float_as_uint(T)))
-    argmin_teams<SMEM, true>(P, smem_u32(smem), T, g);
-  else
-    argmin_teams<SMEM, false>(P, smem_u32(smem), T, g);
+  const uint32_t sb = smem_u32(smem), rb = sb + 4u * padded;
+  // R23: with 2^-40 <= T <= 2^60 every eligible t > 0 is >= 2^-64 and every quotient is 0 or
+  // >= 2^-24, so the reciprocal division stays clear of underflow and overflow
+  const bool fastdiv = SMEM && T >= 0x1p-40f && T <= 0x1p60f;
+  const bool fold = can_fold(__float_as_uint(T));
+  if (fastdiv) {
+    if (fold)
+      argmin_teams<SMEM, true, true>(P, sb, rb, T, g);
+    else
+      argmin_teams<SMEM, false, true>(P, sb, rb, T, g);
+  } else {
+    if (fold)
+      argmin_teams<SMEM, true, false>(P, sb, rb, T, g);
+    else
+      argmin_teams<SMEM, false, false>(P, sb, rb, T, g);
+  }
 }
 
 }  // namespace
 
 cudaError_t launch_argmin_shared(const SharedParams& p, bool smem, int grid, int block, cudaStream_t st) {
   if (smem) {
-    const size_t sh = (size_t)((p.M + 3u) & ~3u) * 4u;
+    const size_t sh = (size_t)((p.M + 3u) & ~3u) * 8u;  // alpha and its reciprocals
     argmin_shared_kernel<true><<<grid, block, sh, st>>>(p);
   } else {
     argmin_shared_kernel<false><<<grid, block, 0, st>>>(p);
