@@ -273,6 +273,20 @@ def test_rows_parity(M, K):
     np.testing.assert_allclose(d, ref["a0"], rtol=1e-6)
 
 
+@pytest.mark.parametrize("warps,stages,log2_block", [(24, 2, 0), (24, 2, 5), (16, 4, 3), (20, 1, 1), (32, 1, 2)])
+def test_rows_pipeline_shapes(monkeypatch, warps, stages, log2_block):
+    # other ring depths, warp counts and row-block sizes of the matrix kernel (the per-warp
+    # row count, the 32-bit walk and the block flush) against the oracle, with a ragged K
+    monkeypatch.setenv("GPUAR_ROWS_WARPS", str(warps))
+    monkeypatch.setenv("GPUAR_ROWS_STAGES", str(stages))
+    monkeypatch.setenv("GPUAR_ROWS_LOG2_BLOCK", str(log2_block))
+    for M, K in [(1029, 30_001), (37, 4099)]:
+        sel, out, ref, (amax, a0) = _rows_case(M, K, k0=12_345, epoch=3)
+        sel.sync()
+        _check(out, ref)
+        np.testing.assert_array_equal(amax.cpu().numpy(), ref["amax"])
+
+
 def test_rows_padded_pitch_and_offset():
     sel, out, ref, _ = _rows_case(1029, 999, ld=1036, k0=12345, epoch=5)
     _check(out, ref)
