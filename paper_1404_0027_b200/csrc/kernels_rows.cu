@@ -10,10 +10,11 @@
 //    bulk async copy, cp.async.bulk -> SASS UBLKCP, of the row's 16-byte-aligned cover)
 //    and consumer, so a slow row (geometric trial count) never stalls another warp;
 //  * rows are streamed with an L2 evict_first policy (read exactly once);
-//  * per row: warp-wide max of the bit patterns (exact alpha_max + validity) and
-//    alpha_0 as binary32 pairwise sums of 8 promoted to binary64 (error <= 4u relative,
-//    DESIGN.md R11), then trials in rounds of 32 Philox calls = 64 trials per warp with a
-//    ballot/__ffs first-accept, then tau with -ln(u1) precomputed 32 rows at a time.
+//  * per row: warp-wide max of the bit patterns (exact alpha_max + validity) and alpha_0
+//    by row_reduce (binary32 pairwise sums of 16 per lane promoted to binary64, error <= 8u
+//    relative, R11), then trials in rounds of 32 Philox calls = 64 trials per
+//    warp with a ballot/__ffs first-accept; -ln(u1) is drawn 32 rows at a time and tau is
+//    formed once per block of rows at the output flush.
 // Row 4116 bytes is not a multiple of 16, so no 2-D tensor map can describe the matrix;
 // each row's copy covers [floor16(start), ceil16(end)) -- at most 15 extra bytes on
 // each side, always inside 16-byte chunks that hold row data.
