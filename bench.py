@@ -30,6 +30,12 @@ sys.path.insert(0, ROOT)
 
 METRIC = "next-reaction selections/sec at 1/2/4/8 B200; % of ALU/HBM roofline"
 UNIT = "selections/s"
+SSA_UNIT = "SSA events/s (one selection each)"
+
+
+def unit_of(w: dict) -> str:
+    """The metric's unit for a workload: SSA events for s1, selections otherwise."""
+    return SSA_UNIT if w["kind"] == "ssa" else UNIT
 # ALU roofline (DESIGN.md §5): the fma pipe takes one warp instruction per 2 cycles per SMSP
 # (B300_MICROARCH.md "Pipe rates", rt_SMSP = 2) = 64 lane-slots/clk/SM; a Philox4x32-10 call
 # is 20 mul.wide.u32 = 20 IMAD.WIDE.U32 (SASS), each writing a register pair = 2 slots.
@@ -300,12 +306,12 @@ def run_reference(args, w, rank, world):
     value = units / dt
     sample = f"{n} of the {w['K']} selections per step ({'rows' if w['kind'] == 'rows' else 'selections'} 0..{n - 1})"
     out = {
-        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+        "impl": "reference", "metric": METRIC, "value": value, "unit": unit_of(w), "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": dt / args.steps * 1e3,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
         "data": "synthetic", "config": {"workload": w["desc"], "M": w["M"], "K_per_gpu": w["K"]},
-        "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "oracle", "sample": sample},
-        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "cpu_baseline": {"value": value, "unit": unit_of(w), "cores": threads, "kind": "oracle", "sample": sample},
+        "e2e": {"value": value, "unit": unit_of(w), "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(out), flush=True)
 
@@ -588,9 +594,9 @@ def run_ssa(args, w, rank, world, local_rank):
         if world == 1 and not args.no_cpu:
             threads = os.cpu_count() or 1
             rate, nn, dt = oracle_rate(w, args.cpu_seconds, threads)
-            cpu = {"value": rate, "unit": "SSA events/s", "cores": threads, "kind": "oracle",
+            cpu = {"value": rate, "unit": SSA_UNIT, "cores": threads, "kind": "oracle",
                    "sample": f"{nn} realizations x {inner} steps from the initial state ({dt:.1f} s)"}
-        res = {"metric": METRIC, "value": value, "unit": "SSA events/s (one selection each)", "n_gpus": world,
+        res = {"metric": METRIC, "value": value, "unit": SSA_UNIT, "n_gpus": world,
                "steps": args.steps, "warmup": max(args.warmup, 3), "ms_per_step": ms / args.steps,
                "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
                "data": "synthetic (seeded synth/ network and initial state)",
