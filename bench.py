@@ -448,7 +448,7 @@ def run_gpuar(args, w, rank, world, local_rank):
         e2e = {"value": K * world * args.e2e_steps / dt_max, "unit": UNIT,
                "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": 12 * K, "steps": args.e2e_steps,
                # the bound of this number: host<->device bytes per second through PCIe
-               "pcie_gbs": (h2d + 12 * K) * args.e2e_steps / dt_max / 1e9,
+               "pcie_gbs_per_rank": (h2d + 12 * K) * args.e2e_steps / dt_max / 1e9,
                "timer": "host wall clock around synchronous gpuar_select_host, max over ranks"}
         del host
 
