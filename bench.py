@@ -492,6 +492,11 @@ def run_gpuar(args, w, rank, world, local_rank):
         cpu = {"value": rate, "unit": UNIT, "cores": threads, "kind": "oracle",
                "sample": f"first {n} of {K} selections of the same workload, re-run on successive epochs "
                          f"for {dt:.1f} s (OpenMP over selections)"}
+        # the same oracle on one host thread (a shorter sample)
+        rate1, n1, dt1 = oracle_rate(w, min(3.0, args.cpu_seconds), 1,
+                                     max_rows=(1 << 14) if w["kind"] == "rows" else None)
+        cpu["value_1thread"] = rate1
+        cpu["sample_1thread"] = f"first {n1} selections, {dt1:.1f} s, one thread"
 
     if rank == 0:
         res = {
