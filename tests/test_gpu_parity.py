@@ -111,15 +111,24 @@ def test_group_max_path_uniform():
     _check(out, ref)
 
 
-def test_bf16_bracket_boundaries():
-    # values exactly on / around bf16 grid points exercise every branch of the bracket
+def test_bracket16_boundaries():
+    # path 2 (16-bit threshold brackets B_j = min(T_j >> 8, 65535)): alpha_max = 2 (a power of
+    # two, so u * alpha_max is exact) and alpha_j = n 2^-15 give T_j = 256 n exactly, i.e.
+    # brackets on their boundaries; alpha_j = alpha_max saturates B_j (T_j = 2^24); plus
+    # bf16-grid values, values just below them, and zeros
     rng = np.random.default_rng(3)
-    base = rng.integers(0x3F000000, 0x40000000, size=70_000, dtype=np.uint32)
-    base[::3] &= 0xFFFF0000            # exactly representable in bf16
-    base[1::7] |= 0x0000FFFF           # just below the next bf16
-    a = base.view(np.float32).copy()
+    M = 70_000
+    n = rng.integers(1, 65536, size=M).astype(np.float64)
+    a = (n * 2.0 ** -15).astype(np.float32)
+    a[::5] = 2.0
+    grid = rng.integers(0x3F000000, 0x3FFFFFFF, size=M, dtype=np.uint32)
+    grid[::2] &= 0xFFFF0000                     # exactly representable in bf16
+    grid[1::2] |= 0x0000FFFF                    # just below the next bf16
+    sel_grid = np.arange(M) % 7 == 3
+    a[sel_grid] = grid[sel_grid].view(np.float32)
     a[::11] = 0.0
-    sel, out, ref = _shared_case(a, 30_000)
+    assert a.max() == 2.0
+    sel, out, ref = _shared_case(a, 40_000)
     assert sel.path == "smem_bracket16"
     _check(out, ref)
 
@@ -188,7 +197,7 @@ def test_extreme_scales_thresholds(scale_exp):
     _check(out, ref)
 
 
-def test_thresholds_on_bf16_and_grid_values():
+def test_thresholds_on_grid_values():
     # exact powers of two, values one ulp apart and alpha_j == alpha_max on path 1
     a = np.array([1.0, np.nextafter(np.float32(1.0), np.float32(0)), 0.5, 0.25 + 2 ** -25, 2 ** -24, 2 ** -25,
                   0.0, 1.0, 0.75, np.float32(1) - np.float32(2 ** -24)], dtype=np.float32)
