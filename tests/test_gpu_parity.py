@@ -133,6 +133,19 @@ def test_bracket16_boundaries():
     _check(out, ref)
 
 
+def test_group_bounds_on_boundaries():
+    # path 3 (per-group bounds G = min(ceil(max T_j / 256), 65535)): T_j = 256 n exactly
+    # (alpha_max = 2, alpha_j = n 2^-15), saturated groups (alpha_j = alpha_max) and zeros
+    rng = np.random.default_rng(5)
+    M = 600_000
+    a = (rng.integers(1, 65536, size=M).astype(np.float64) * 2.0 ** -15).astype(np.float32)
+    a[::997] = 2.0
+    a[rng.random(M) < 0.3] = 0.0
+    sel, out, ref = _shared_case(a, 20_000)
+    assert sel.path == "smem_group_max"
+    _check(out, ref)
+
+
 def test_degenerate_and_single_nonzero():
     _, out, ref = _shared_case([0, 0, 0, 0, 0], 1000)
     _check(out, ref)
