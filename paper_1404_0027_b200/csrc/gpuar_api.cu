@@ -71,7 +71,7 @@ struct gpuar_handle {
   int num_sms = 148;
   int smem_optin = 227 * 1024;
   // rows policy
-  int rows_warps = 0, rows_stages = 0, rows_grid = 0, rows_lb = 2;
+  int rows_warps = 0, rows_stages = 0, rows_grid = 0, rows_lb = 3;
   uint32_t stage_bytes = 0;
   // shared policy
   int sh_block = 256, sh_grid = 0;
@@ -174,7 +174,7 @@ int plan_rows(gpuar_handle* h) {
   if (!fits(W, S)) return GPUAR_EINVAL;  // M too large for the row pipeline
   h->rows_warps = W;
   h->rows_stages = S;
-  h->rows_lb = std::max(0, std::min(5, env_int("GPUAR_ROWS_LOG2_BLOCK", 2)));
+  h->rows_lb = std::max(0, std::min(5, env_int("GPUAR_ROWS_LOG2_BLOCK", 3)));  // B = 8 (r01 A/B)
   h->stage_bytes = (uint32_t)sb;
   const size_t sh = (((size_t)W * S * 8u + 127u) & ~(size_t)127u) + (size_t)W * S * sb;
   const int n = select_rows_blocks_per_sm(W, sh);

@@ -114,7 +114,7 @@ __global__ void __launch_bounds__(MAXW * 32, 1) select_rows_kernel(const RowsPar
   const unsigned char* base = reinterpret_cast<const unsigned char*>(P.alpha);
   // Rows of this warp: warps take turns on blocks of B = 2^lb consecutive rows (block
   // b = wg, wg + WT, ...), so the rows in flight over the whole GPU stay within a window of
-  // B*WT rows (B = 4: ~58 MB, inside the 256 MB TLB reach) while a warp's outputs for a
+  // B*WT rows (B = 8: ~117 MB, inside the 256 MB TLB reach) while a warp's outputs for a
   // block go out as one store per output array from B lanes.  The warp's row count is fixed
   // up front, so the walk below never compares row indices against K.
   const uint32_t WT = gridDim.x * warps;
