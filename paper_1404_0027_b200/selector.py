@@ -19,6 +19,17 @@ def _ptr(t: torch.Tensor | None):
     return None if t is None else ctypes.c_void_p(t.data_ptr())
 
 
+# The current stream's raw cudaStream_t for a device index: torch's own fast accessor when
+# present (a plain int, ~10x cheaper than building a torch.cuda.Stream), else the public API.
+_raw_stream = getattr(torch._C, "_cuda_getCurrentRawStream", None)
+
+
+def _current_stream_ptr(device: torch.device) -> int:
+    if _raw_stream is not None:
+        return int(_raw_stream(device.index))
+    return torch.cuda.current_stream(device).cuda_stream
+
+
 class Selector:
     """GPU-AR selector for M reactions and up to K selections per call (gpuar_create).
 
@@ -66,7 +77,7 @@ class Selector:
         self.close()
 
     def _stream(self) -> None:
-        s = torch.cuda.current_stream(self.device).cuda_stream
+        s = _current_stream_ptr(self.device)
         if s != self._last_stream:  # gpuar_set_stream orders the new stream after the old one
             check(self._lib.gpuar_set_stream(self._h, ctypes.c_void_p(s)), "gpuar_set_stream")
             self._last_stream = s
@@ -142,9 +153,13 @@ class Selector:
             trials = torch.empty(K, dtype=torch.int32, device=self.device) if with_trials else None
         else:
             idx, tau, trials = out
-        # (no torch device context: the library switches to the handle's device itself)
+        # (no torch device context: the library switches to the handle's device itself;
+        # raw integer addresses: ctypes converts them for the void* parameters)
         self._stream()
-        check(self._lib.gpuar_select(self._h, K, _ptr(idx), _ptr(tau), _ptr(trials)), "gpuar_select")
+        st = self._lib.gpuar_select(self._h, K, idx.data_ptr(), None if tau is None else tau.data_ptr(),
+                                    None if trials is None else trials.data_ptr())
+        if st:
+            check(st, "gpuar_select")
         return idx, tau, trials
 
     def select_host(self, alpha: np.ndarray | torch.Tensor, K: int | None = None, out: tuple | None = None):
