@@ -361,7 +361,14 @@ __global__ void __launch_bounds__(1024, 1) select_shared_kernel(const SharedPara
   // selection per team; tickets are prefetched one chunk ahead.
   const unsigned long long teams = 32u / g;
   const unsigned long long fair = max(1ull, (unsigned long long)K / nwarps);
-  const unsigned long long first = max(teams, fair / 2ull);
+  unsigned long long first = max(teams, fair / 2ull);
+  if (fair <= 4ull) {
+    // a few selections per warp: static chunks that cover each stripe, no tickets at all
+    // (the atomic's round trip would cost more than any imbalance it evens out)
+    const unsigned long long stripe = ((unsigned long long)K + kStripes - 1) / kStripes;
+    const unsigned long long per = max(1u, nwarps / kStripes);  // fewest warps any stripe has
+    first = max(teams, (stripe + per - 1) / per);
+  }
   // (r01 sweep, GPUAR_GRAB: c2 best at 2 with prefetch; heavy tails (st.grab = 1) at 1)
   unsigned long long grab = max(teams, min((unsigned long long)st.grab, max(2ull * teams, fair / 8ull)));
   if (P.grab_override) grab = P.grab_override;
