@@ -91,7 +91,8 @@ int gpuar_set_stream(gpuar_t h, void *stream);
  *               D[r*ld + j]) belongs to local selection r; its
  *               alpha_max / alpha_0 are reduced inside gpuar_select.  d_alpha must be
  *               16-byte aligned (rows are streamed with 1-D bulk async copies).
- * Errors: EINVAL (NULL pointer, rows not in {1, K}, ld < M, misaligned matrix base),
+ * Errors: EINVAL (NULL pointer, rows not in {1, K}, ld < M, misaligned matrix base, or
+ * a matrix whose row cannot fit one shared-memory ring slot: M > 57 000 on B200),
  * ENOMEM, ECUDA.  Invalid values are reported later as sticky EPROPENSITY. */
 int gpuar_set_propensities(gpuar_t h, const float *d_alpha, int64_t rows, int64_t ld);
 

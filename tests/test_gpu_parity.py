@@ -309,6 +309,15 @@ def test_rows_pipeline_shapes(monkeypatch, warps, stages, log2_block):
         np.testing.assert_array_equal(amax.cpu().numpy(), ref["amax"])
 
 
+def test_rows_too_wide_for_the_ring_is_refused():
+    from paper_1404_0027_b200 import GpuarError
+    M, K = 60_000, 4
+    sel = _sel(M, K)
+    with pytest.raises(GpuarError) as e:
+        sel.set_propensities(torch.ones((K, M), device="cuda"))
+    assert e.value.status == -1
+
+
 def test_rows_padded_pitch_and_offset():
     sel, out, ref, _ = _rows_case(1029, 999, ld=1036, k0=12345, epoch=5)
     _check(out, ref)
