@@ -54,6 +54,43 @@ __device__ __forceinline__ void row_trials(const Stream& ts, uint32_t sel, uint3
   }
 }
 
+// N Philox calls' reactions 4c_i..4c_i+3 (FULL: all < M, else bounds-tested), calls in
+// increasing order.  The common case -- none of the 4N eligible (probability (1 - p)^4N) --
+// costs the loads, uniforms and compares and ONE branch, and with N = 2 the two calls'
+// independent IMAD.WIDE chains interleave (24 warps per SM do not hide one chain's
+// latency); the division and the minimum update run only for an eligible reaction (an
+// ineligible one rates 1.0, which never beats bestR).
+template <int N, bool FOLD, bool FULL>
+__device__ __forceinline__ void rate_calls(const Philox4 (&x)[N], const uint32_t (&c)[N], uint32_t row_s, uint32_t M,
+                                           float T, float T_s, float& bestR, uint32_t& bestJ) {
+  float d[4 * N], t[4 * N];
+  bool e[4 * N];
+  bool any = false;
+#pragma unroll
+  for (int i = 0; i < N; ++i) {
+    const uint32_t a = row_s + 16u * c[i];
+    const uint32_t xs[4] = {x[i].x, x[i].y, x[i].z, x[i].w};
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      d[4 * i + q] = lds_f32(a + 4u * q);
+      // a leftover call may be the row's partial one: reactions >= M do not exist
+      if (!FULL && q > 0) d[4 * i + q] = 4u * c[i] + q < M ? d[4 * i + q] : 0.f;
+      t[4 * i + q] = scaled_u<FOLD>(xs[q], T, T_s);
+      e[4 * i + q] = t[4 * i + q] < d[4 * i + q];
+      any |= e[4 * i + q];
+    }
+  }
+  if (any) {
+#pragma unroll
+    for (int k = 0; k < 4 * N; ++k) {
+      if (e[k]) {  // increasing j with a strict `<`: the lowest index keeps a tied rating
+        const float R = __fdiv_rn(t[k], d[k]);
+        if (R < bestR) bestR = R, bestJ = 4u * c[k >> 2] + (k & 3);
+      }
+    }
+  }
+}
+
 // The paper's printed rule on one row (R16-R19): lane l rates reactions 4c..4c+3
 // of its calls c = l, l+32, ...; warp butterfly on the (rating bits, index) key.
 template <bool FOLD, class Stream>
@@ -61,23 +98,23 @@ __device__ __forceinline__ void row_argmin(const Stream& ts, uint32_t sel, uint3
                                            uint32_t lane, int32_t& id) {
   const float T_s = __fmul_rn(T, 0x1p-24f);
   const uint32_t k1t = ts.rk1[0] ^ kTagElection;
+  const uint32_t full = M >> 2;  // calls whose four reactions all exist
   const uint32_t calls = (M + 3u) >> 2;
   float bestR = 1.0f;  // lane-local minimum; a lane sees its j in increasing order
   uint32_t bestJ = 0xffffffffu;
-  for (uint32_t c = lane; c < calls; c += 32u) {
-    const Philox4 x = ts.with_tag(c, sel, k1t);
-    const uint32_t xs[4] = {x.x, x.y, x.z, x.w};
-#pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      const uint32_t j = 4u * c + q;
-      const float d = j < M ? lds_f32(row_s + 4u * j) : 0.f;
-      const float t = scaled_u<FOLD>(xs[q], T, T_s);
-      const float R = (t < d) ? __fdiv_rn(t, d) : 1.0f;
-      if (R < bestR) {
-        bestR = R;
-        bestJ = j;
-      }
-    }
+  // two full calls per iteration
+  uint32_t c = lane;
+  for (; c + 32u < full; c += 64u) {
+    const Philox4 x[2] = {ts.with_tag(c, sel, k1t), ts.with_tag(c + 32u, sel, k1t)};
+    const uint32_t cc[2] = {c, c + 32u};
+    rate_calls<2, FOLD, true>(x, cc, row_s, M, T, T_s, bestR, bestJ);
+  }
+  // the leftover calls (at most two per lane; at M = 1029 lane 0 has call 256 and lane 1
+  // the partial call 257) in ONE predicated step, so the warp pays one Philox latency
+  for (; c < calls; c += 32u) {
+    const Philox4 x[1] = {ts.with_tag(c, sel, k1t)};
+    const uint32_t cc[1] = {c};
+    rate_calls<1, FOLD, false>(x, cc, row_s, M, T, T_s, bestR, bestJ);
   }
   unsigned long long best = ((unsigned long long)__float_as_uint(bestR) << 32) | bestJ;
 #pragma unroll
