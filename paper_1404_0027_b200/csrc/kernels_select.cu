@@ -206,7 +206,10 @@ __device__ __forceinline__ void trial_loop(const SharedParams& P, const TrialStr
 
 // One lane per selection (g = 1, high p): every round each lane makes one Philox call for
 // its own selection; a lane that finishes stores its result and takes the next selection of
-// the warp's pool (one ballot + popc), with no cross-lane data exchange.
+// the warp's pool (one ballot + popc), with no cross-lane data exchange.  At high p most
+// rounds finish some lane, so the hand-out has a fast path: the current chunk covers every
+// idle lane -> one popc and a 32-bit add (selection indices are < K < 2^32); only a chunk
+// boundary takes the general loop (refill / prefetch).
 template <int PATH>
 __device__ __forceinline__ void lane_loop(const SharedParams& P, const TrialStream& ts, uint32_t sbase, Pool pl) {
   const uint32_t M = P.M;
@@ -214,26 +217,42 @@ __device__ __forceinline__ void lane_loop(const SharedParams& P, const TrialStre
   const uint32_t calls = half + (P.max_trials & 1u);
   const uint32_t lane = threadIdx.x & 31u;
   const uint32_t lt = lanemask_lt();
+  const uint32_t s0 = P.s0;
+  int32_t* const idx_out = P.idx;
+  uint32_t* const tr_out = P.trials;
+  const bool want_tr = tr_out != nullptr;
   uint32_t my = kNone, sel = 0, c = 0;
   bool active = false;
   uint32_t need = kFull;  // lanes without a selection
   while (true) {
     if (need != 0u) {  // warp-uniform: hand out selections
-      while (need != 0u && !pl.exhausted) {
-        if (pl.next >= pl.end && !pl.refill(lane)) break;
-        const uint32_t avail = (uint32_t)(pl.end - pl.next);
-        const uint32_t r = __popc(need & lt);
-        const bool mine = ((need >> lane) & 1u) && r < avail;
-        if (mine) {
-          my = (uint32_t)pl.next + r;
-          sel = ts.sel_word(P.s0 + my);
+      const uint32_t n = __popc(need);
+      const uint32_t nx = (uint32_t)pl.next;
+      if (pl.next < pl.end && (uint32_t)pl.end - nx >= n) {  // fast path: the chunk covers all
+        if (!active) {
+          my = nx + __popc(need & lt);
+          sel = ts.sel_word(s0 + my);
           c = 0;
           active = true;
         }
-        pl.next += min((uint32_t)__popc(need), avail);
-        need &= ~__ballot_sync(kFull, mine);
+        pl.next = nx + n;
+      } else {
+        while (need != 0u && !pl.exhausted) {
+          if (pl.next >= pl.end && !pl.refill(lane)) break;
+          const uint32_t avail = (uint32_t)(pl.end - pl.next);
+          const uint32_t r = __popc(need & lt);
+          const bool mine = ((need >> lane) & 1u) && r < avail;
+          if (mine) {
+            my = (uint32_t)pl.next + r;
+            sel = ts.sel_word(s0 + my);
+            c = 0;
+            active = true;
+          }
+          pl.next += min((uint32_t)__popc(need), avail);
+          need &= ~__ballot_sync(kFull, mine);
+        }
+        if (pl.exhausted && !__any_sync(kFull, active)) break;
       }
-      if (pl.exhausted && !__any_sync(kFull, active)) break;
     }
     const Philox4 x = ts(c, sel);
     const uint32_t j0 = __umulhi(x.x, M);
@@ -244,8 +263,8 @@ __device__ __forceinline__ void lane_loop(const SharedParams& P, const TrialStre
     const bool a1 = (c < half) & r1;
     const bool done = active & (a0 | a1 | (c + 1u >= calls));
     if (done) {
-      P.idx[my] = a0 ? (int32_t)j0 : (a1 ? (int32_t)j1 : -1);
-      if (P.trials) P.trials[my] = a0 ? 2u * c + 1u : (a1 ? 2u * c + 2u : P.max_trials);
+      idx_out[my] = a0 ? (int32_t)j0 : (a1 ? (int32_t)j1 : -1);
+      if (want_tr) tr_out[my] = a0 ? 2u * c + 1u : (a1 ? 2u * c + 2u : P.max_trials);
       active = false;
     }
     ++c;
