@@ -486,6 +486,35 @@ def test_argmin_rows():
         assert rel.max() <= TAU_RTOL
 
 
+@pytest.mark.parametrize("M", [1, 2, 3, 4, 5, 31, 63, 64, 65, 95, 128, 130, 257, 1030, 1031, 1032, 4099])
+def test_argmin_rows_shapes(M):
+    """The row kernel's argmin branch at every M mod 4 and around the 32/64-call loop edges
+    (pair loop, leftover calls, partial call), on rows where eligibility is rare (yeast-like
+    enable mask: the division path is the exception) and common (discrete Gaussian: most
+    reactions eligible), plus an all-zero row and a one-reaction row."""
+    K = 700
+    rng = np.random.default_rng(1000 + M)
+    sparse = synth.rows(synth.yeast_rates(max(M, 2))[:M].copy(), synth.GEN_SEED, 0, K // 2)
+    dense = np.tile(synth.discrete_gaussian(M) if M > 5 else np.arange(1, M + 1, dtype=np.float32),
+                    (K - K // 2, 1))
+    dense *= rng.uniform(0.5, 2.0, size=(dense.shape[0], 1)).astype(np.float32)
+    host = np.ascontiguousarray(np.vstack([sparse, dense]).astype(np.float32))
+    host[3, :] = 0.0
+    host[4, :] = 0.0
+    host[4, M // 2] = 3.0
+    for w in (1.0, 1.7):
+        sel = _sel(M, K)
+        sel.set_rule("argmin", w)
+        sel.set_propensities(torch.from_numpy(host).cuda())
+        idx, tau, trials = sel.select(K)
+        sel.sync()
+        ref = oracle.argmin_select(host, K, seed=SEED, w=w, nthreads=8)
+        np.testing.assert_array_equal(idx.cpu().numpy(), ref["idx"])
+        assert idx[3].item() == -1
+        # every draw of a row is consumed; an all-zero row draws nothing
+        np.testing.assert_array_equal(trials.cpu().numpy(), np.where(host.any(axis=1), M, 0))
+
+
 def test_set_rule_validation():
     from paper_1404_0027_b200 import GpuarError
     sel = _sel(4, 4)
