@@ -68,8 +68,7 @@ __device__ __forceinline__ void argmin_teams(const SharedParams& P, uint32_t sba
     const uint32_t sel = ts.sel_word(P.s0 + s);
     float bestR = 1.0f;  // sentinel: nothing eligible yet
     uint32_t bestJ = 0xffffffffu;
-    for (uint32_t c = rank; c < calls; c += g) {
-      const Philox4 x = ts(c, sel);
+    auto rate = [&](uint32_t c, const Philox4& x) {
       const uint32_t j = 4u * c;
       float4 d, y = make_float4(0.f, 0.f, 0.f, 0.f);
       if constexpr (SMEM) {
@@ -85,7 +84,16 @@ __device__ __forceinline__ void argmin_teams(const SharedParams& P, uint32_t sba
       elect<FASTDIV>(scaled_u<FOLD>(x.y, T, T_s), d.y, y.y, j + 1u, bestR, bestJ);
       elect<FASTDIV>(scaled_u<FOLD>(x.z, T, T_s), d.z, y.z, j + 2u, bestR, bestJ);
       elect<FASTDIV>(scaled_u<FOLD>(x.w, T, T_s), d.w, y.w, j + 3u, bestR, bestJ);
+    };
+    // two calls per iteration: independent IMAD.WIDE chains interleave; rated in call order
+    uint32_t c = rank;
+    for (; c + g < calls; c += 2u * g) {
+      const Philox4 xa = ts(c, sel);
+      const Philox4 xb = ts(c + g, sel);
+      rate(c, xa);
+      rate(c + g, xb);
     }
+    if (c < calls) rate(c, ts(c, sel));
     // team minimum of the lexicographic (rating bits, index) key
     unsigned long long best = ((unsigned long long)__float_as_uint(bestR) << 32) | bestJ;
     for (uint32_t o = g >> 1; o > 0; o >>= 1) best = min(best, __shfl_xor_sync(kFull, best, o));
