@@ -58,6 +58,7 @@ struct gpuar_handle {
   DevCounters* d_ctr = nullptr;
   uint32_t ticket_phase = 0;  // DevCounters::next set of the next shared-vector launch
   uint32_t grab_override = 0; // tuning knobs, read from the environment once at create time
+  uint32_t team_override = 0;
   uint32_t no_prefetch = 0;
   double* d_part_sum = nullptr;
   uint32_t* d_part_max = nullptr;
@@ -208,6 +209,7 @@ int launch_select(gpuar_handle* h, const float* alpha, int64_t rows, int64_t ld,
     p.smem_bytes = h->shared_smem;
     p.w = h->w;
     p.grab_override = h->grab_override;
+    p.team_override = h->team_override;
     p.no_prefetch = h->no_prefetch;
     if (h->rule == kRuleArgmin) {
       e = launch_argmin_shared(p, h->am_smem, h->am_grid, 256, st);
@@ -328,6 +330,10 @@ int gpuar_create(gpuar_t* out, int64_t M, int64_t K, uint64_t seed) {
   h->stats_blocks = (int)std::min<int64_t>((M + 4095) / 4096, 512);
   plan_shared(h);
   h->grab_override = (uint32_t)std::max(0, env_int("GPUAR_GRAB", 0));
+  {
+    const int g = env_int("GPUAR_TEAM", 0);  // 1, 2, 4, ..., 32 (else the model decides)
+    h->team_override = (g >= 1 && g <= 32 && (g & (g - 1)) == 0) ? (uint32_t)g : 0u;
+  }
   h->no_prefetch = (uint32_t)std::max(0, env_int("GPUAR_NO_PREFETCH", 0));
   cudaError_t e = cudaMalloc(&h->d_stats, sizeof(DevStats));
   if (e == cudaSuccess) e = cudaMalloc(&h->d_ctr, sizeof(DevCounters));

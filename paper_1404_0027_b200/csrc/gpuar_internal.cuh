@@ -66,6 +66,7 @@ struct SharedParams {
   uint32_t smem_bytes;       // bytes of the staged vector / prefilter
   float w;                   // argmin rule: T = fl32(w * alpha_max)
   uint32_t grab_override;    // tuning: fixed selections per ticket grab (0 = model)
+  uint32_t team_override;    // tuning: fixed team size g (power of two 1..32; 0 = model)
   uint32_t no_prefetch;      // tuning: 1 = fetch tickets on demand
   uint32_t phase;            // ticket set of this launch (DevCounters::next)
 };

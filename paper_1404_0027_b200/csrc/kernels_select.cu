@@ -355,7 +355,7 @@ __global__ void __launch_bounds__(1024, 1) select_shared_kernel(const SharedPara
   const bool zero = st.amax_bits == 0u;
   const uint32_t K = P.K;
   const uint32_t nwarps = nthreads >> 5;
-  if (threadIdx.x == 0) s_g = choose_team(st.p, K, nwarps);  // once per CTA, not per warp
+  if (threadIdx.x == 0) s_g = P.team_override ? P.team_override : choose_team(st.p, K, nwarps);  // once per CTA
 
   // ---- phase A: tau for every selection; degenerate / invalid outputs
   for (uint32_t s = tid; s < K; s += nthreads) {

@@ -52,6 +52,15 @@ def main():
     idx, _, _ = sel.select(K)
     sel.sync()
     check(idx.cpu().numpy(), oracle.argmin_select(host, K, seed=SEED, epoch=1, nthreads=8)["idx"], "rows argmin")
+    # argmin rows: the partial last call reads past M inside the ring slot (masked)
+    for Mo in (5, 1030, 1031):
+        ho = synth.rows(synth.yeast_rates(Mo), synth.GEN_SEED, 0, 300)
+        so = Selector(Mo, 300, SEED)
+        so.set_rule("argmin", 1.0)
+        so.set_propensities(torch.from_numpy(ho).cuda())
+        io, _, _ = so.select(300)
+        so.sync()
+        check(io.cpu().numpy(), oracle.argmin_select(ho, 300, seed=SEED, nthreads=8)["idx"], f"rows argmin M={Mo}")
     # host pipeline
     sel = Selector(M, K, SEED)
     hi, _, _ = sel.select_host(torch.from_numpy(host).pin_memory())
