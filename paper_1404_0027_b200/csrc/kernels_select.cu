@@ -314,8 +314,11 @@ __device__ __forceinline__ void warp_loop(const SharedParams& P, const TrialStre
 // Team size g (power of two, 1..32) minimising the estimated warp instructions per
 // selection (E = 1/p expected trials; SASS counts of the r01 build):
 //   g = 32 (warp_loop): (E/64 + 1/2) rounds x 62 + 15 per selection;
-//   g = 1 (lane_loop): (E + 1)/64 warp-rounds x (72 + 15 P(any lane of the warp finished));
-//   1 < g < 32 (trial_loop): (E + g)/64 warp-rounds x (67 + 55 P(any lane finished));
+//   g = 1 (lane_loop): (E + 1)/64 warp-rounds x (72 + 45 P(any lane of the warp finished));
+//   1 < g < 32 (trial_loop): (E + g)/64 warp-rounds x (67 + 45 P(any lane finished));
+// (finish costs recalibrated in session 2: ncu counts ~125 warp instructions per lane-loop
+// round when a lane finishes almost every round (c3 exponential, M = 10^4), and the
+// GPUAR_TEAM sweep has g = 4 fastest at E ~ 73 (c3 Pareto, M = 10^3));
 // times (1 + drain tail), tail = 0.1 T ln(T+1) * warps / K with T = 32/g teams per warp.
 // (The 0.1 is the session-2 team sweep, GPUAR_TEAM: at K = 10^4 the unscaled tail chose
 // g = 32 where g = 4 runs 5 % faster; at K >= 2^16 the tail is too small to move a choice.)
@@ -328,7 +331,7 @@ __device__ __forceinline__ uint32_t choose_team(float p, uint32_t K, uint32_t nw
   best_cost *= 1.0f + 0.06931f * wk;
   for (uint32_t g = 1u; g < 32u; g <<= 1) {
     const float T = (float)(32u / g);
-    const float round = (g == 1u) ? 72.0f + 15.0f * any : 67.0f + 55.0f * any;
+    const float round = (g == 1u) ? 72.0f + 45.0f * any : 67.0f + 45.0f * any;
     const float cost = (E + (float)g) / 64.0f * round * (1.0f + 0.1f * T * __logf(T + 1.0f) * wk);
     if (cost < best_cost) {
       best_cost = cost;
