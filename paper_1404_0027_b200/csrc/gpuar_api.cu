@@ -59,6 +59,7 @@ struct gpuar_handle {
   uint32_t ticket_phase = 0;  // DevCounters::next set of the next shared-vector launch
   uint32_t grab_override = 0; // tuning knobs, read from the environment once at create time
   uint32_t team_override = 0;
+  bool pdl = true;            // programmatic dependent launch of the shared-vector kernels
   uint32_t no_prefetch = 0;
   double* d_part_sum = nullptr;
   uint32_t* d_part_max = nullptr;
@@ -212,7 +213,7 @@ int launch_select(gpuar_handle* h, const float* alpha, int64_t rows, int64_t ld,
     p.team_override = h->team_override;
     p.no_prefetch = h->no_prefetch;
     if (h->rule == kRuleArgmin) {
-      e = launch_argmin_shared(p, h->am_smem, h->am_grid, 256, st);
+      e = launch_argmin_shared(p, h->am_smem, h->am_grid, 256, st, h->pdl);
     } else if (h->rule == kRuleIT) {
       e = cudaSuccess;
       if (!h->d_prefix) e = cudaMalloc(&h->d_prefix, (sizeof(double) * (size_t)h->M + 15u) & ~(size_t)15);
@@ -221,10 +222,10 @@ int launch_select(gpuar_handle* h, const float* alpha, int64_t rows, int64_t ld,
         h->prefix_valid = e == cudaSuccess;
       }
       const bool smem = (size_t)h->M * 8u + 1024u <= (size_t)h->smem_optin;
-      if (e == cudaSuccess) e = launch_it_select(p, h->d_prefix, smem, h->num_sms * 8, st);
+      if (e == cudaSuccess) e = launch_it_select(p, h->d_prefix, smem, h->num_sms * 8, st, h->pdl);
     } else {
       p.phase = h->ticket_phase;
-      e = launch_select_shared(p, h->shared_path, h->sh_grid, h->sh_block, st);
+      e = launch_select_shared(p, h->shared_path, h->sh_grid, h->sh_block, st, h->pdl);
       if (e == cudaSuccess) h->ticket_phase ^= 1u;
     }
   } else {
@@ -335,6 +336,7 @@ int gpuar_create(gpuar_t* out, int64_t M, int64_t K, uint64_t seed) {
     h->team_override = (g >= 1 && g <= 32 && (g & (g - 1)) == 0) ? (uint32_t)g : 0u;
   }
   h->no_prefetch = (uint32_t)std::max(0, env_int("GPUAR_NO_PREFETCH", 0));
+  h->pdl = env_int("GPUAR_NO_PDL", 0) == 0;
   cudaError_t e = cudaMalloc(&h->d_stats, sizeof(DevStats));
   if (e == cudaSuccess) e = cudaMalloc(&h->d_ctr, sizeof(DevCounters));
   if (e == cudaSuccess) e = cudaMalloc(&h->d_part_sum, sizeof(double) * h->stats_blocks);

@@ -2,6 +2,7 @@
 // by libgpuar's translation units.  Not part of the ABI (include/gpuar.h is).
 #pragma once
 #include <cstdint>
+#include <utility>
 #include <cuda_runtime.h>
 
 namespace gpuar {
@@ -341,17 +342,40 @@ __device__ __forceinline__ void row_reduce(uint32_t row_s, uint32_t M, uint32_t 
   acc_out = acc;
 }
 
+// Programmatic dependent launch (PDL, sm_90+): griddepcontrol.wait blocks until every
+// prerequisite grid of the stream has completed and its memory is visible; launch_dependents
+// lets the next PDL-launched grid be scheduled before this one finishes.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_launch_dependents() { asm volatile("griddepcontrol.launch_dependents;" :::); }
+
+// Launch with (pdl) or without the programmatic-stream-serialization attribute.
+template <class... KArgs, class... Args>
+cudaError_t launch_pdl(void (*kernel)(KArgs...), int grid, int block, size_t smem, cudaStream_t st, bool pdl,
+                       Args&&... args) {
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3((unsigned)grid);
+  cfg.blockDim = dim3((unsigned)block);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
+}
+
 // ---------------------------------------------------------------- launchers (host)
 
 cudaError_t launch_stats(const float* alpha, uint32_t M, double* part_sum, uint32_t* part_max,
                          DevStats* stats, DevCounters* ctr, int stats_blocks, cudaStream_t st);
 cudaError_t launch_thresholds(const float* alpha, uint32_t M, const DevStats* stats, uint32_t* thr, uint16_t* pref,
                               uint32_t n_pref, uint32_t group_shift, int path, cudaStream_t st);
-cudaError_t launch_select_shared(const SharedParams& p, int path, int grid, int block, cudaStream_t st);
-cudaError_t launch_argmin_shared(const SharedParams& p, bool smem, int grid, int block, cudaStream_t st);
+cudaError_t launch_select_shared(const SharedParams& p, int path, int grid, int block, cudaStream_t st, bool pdl);
+cudaError_t launch_argmin_shared(const SharedParams& p, bool smem, int grid, int block, cudaStream_t st, bool pdl);
 void set_argmin_limits(int bytes);
 cudaError_t launch_it_prefix(const float* alpha, uint32_t M, double* C, cudaStream_t st);
-cudaError_t launch_it_select(const SharedParams& p, const double* C, bool smem, int grid, cudaStream_t st);
+cudaError_t launch_it_select(const SharedParams& p, const double* C, bool smem, int grid, cudaStream_t st, bool pdl);
 void set_it_limits(int bytes);
 cudaError_t launch_ssa(const SsaParams& p, int grid, int warps, cudaStream_t st);
 int ssa_blocks_per_sm(int warps, size_t smem);

@@ -108,6 +108,8 @@ __device__ __forceinline__ void argmin_teams(const SharedParams& P, uint32_t sba
 template <bool SMEM>
 __global__ void __launch_bounds__(256) argmin_shared_kernel(const SharedParams P) {
   extern __shared__ __align__(16) unsigned char smem[];
+  pdl_wait();  // programmatic dependent launch: nothing before the previous grids complete
+  pdl_launch_dependents();
   const DevStats st = *P.stats;
   const uint32_t tid = blockIdx.x * blockDim.x + threadIdx.x;
   const uint32_t nthreads = gridDim.x * blockDim.x;
@@ -160,14 +162,12 @@ __global__ void __launch_bounds__(256) argmin_shared_kernel(const SharedParams P
 
 }  // namespace
 
-cudaError_t launch_argmin_shared(const SharedParams& p, bool smem, int grid, int block, cudaStream_t st) {
+cudaError_t launch_argmin_shared(const SharedParams& p, bool smem, int grid, int block, cudaStream_t st, bool pdl) {
   if (smem) {
     const size_t sh = (size_t)((p.M + 3u) & ~3u) * 8u;  // alpha and its reciprocals
-    argmin_shared_kernel<true><<<grid, block, sh, st>>>(p);
-  } else {
-    argmin_shared_kernel<false><<<grid, block, 0, st>>>(p);
+    return launch_pdl(argmin_shared_kernel<true>, grid, block, sh, st, pdl, p);
   }
-  return cudaGetLastError();
+  return launch_pdl(argmin_shared_kernel<false>, grid, block, 0, st, pdl, p);
 }
 
 void set_argmin_limits(int bytes) {

@@ -32,6 +32,8 @@ __global__ void it_prefix_kernel(const float* __restrict__ alpha, uint32_t M, do
 template <bool SMEM>
 __global__ void __launch_bounds__(256) it_select_kernel(const SharedParams P, const double* __restrict__ Cg) {
   extern __shared__ __align__(16) unsigned char smem[];
+  pdl_wait();  // programmatic dependent launch: nothing before the previous grids complete
+  pdl_launch_dependents();
   const double* C = Cg;
   if constexpr (SMEM) {
     __shared__ uint64_t stage_bar;
@@ -77,12 +79,9 @@ cudaError_t launch_it_prefix(const float* alpha, uint32_t M, double* C, cudaStre
   return cudaGetLastError();
 }
 
-cudaError_t launch_it_select(const SharedParams& p, const double* C, bool smem, int grid, cudaStream_t st) {
-  if (smem)
-    it_select_kernel<true><<<grid, 256, ((size_t)p.M * 8u + 15u) & ~(size_t)15, st>>>(p, C);
-  else
-    it_select_kernel<false><<<grid, 256, 0, st>>>(p, C);
-  return cudaGetLastError();
+cudaError_t launch_it_select(const SharedParams& p, const double* C, bool smem, int grid, cudaStream_t st, bool pdl) {
+  if (smem) return launch_pdl(it_select_kernel<true>, grid, 256, ((size_t)p.M * 8u + 15u) & ~(size_t)15, st, pdl, p, C);
+  return launch_pdl(it_select_kernel<false>, grid, 256, 0, st, pdl, p, C);
 }
 
 void set_it_limits(int bytes) {

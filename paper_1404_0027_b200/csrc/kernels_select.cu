@@ -346,6 +346,13 @@ __global__ void __launch_bounds__(1024, 1) select_shared_kernel(const SharedPara
   extern __shared__ __align__(16) unsigned char smem[];
   __shared__ uint64_t stage_bar;
   __shared__ uint32_t s_g;
+  // Programmatic dependent launch: this grid may be resident before the previous kernel of
+  // the stream has finished (its CTAs fill the SM slots freed by that kernel's tail), so
+  // nothing -- not even a read of the thresholds or statistics -- happens before every
+  // prerequisite grid has completed and its writes are visible.  Then let the next launch
+  // be scheduled as early as possible (it waits here in turn).
+  pdl_wait();
+  pdl_launch_dependents();
   // the next launch's ticket set (its previous user, launch n - 1, has completed)
   if (blockIdx.x == 0 && threadIdx.x < kStripes) P.ctr->next[P.phase ^ 1u][threadIdx.x] = 0ull;
   // ---- stage the thresholds (path 1) or their prefilter (paths 2, 3) in smem with one bulk async
@@ -414,22 +421,18 @@ void set_limit(int bytes) {
 
 }  // namespace
 
-cudaError_t launch_select_shared(const SharedParams& p, int path, int grid, int block, cudaStream_t st) {
+cudaError_t launch_select_shared(const SharedParams& p, int path, int grid, int block, cudaStream_t st, bool pdl) {
   const size_t sh = p.smem_bytes;
   switch (path) {
     case kPathSmemF32:
-      select_shared_kernel<kPathSmemF32><<<grid, block, sh, st>>>(p);
-      break;
+      return launch_pdl(select_shared_kernel<kPathSmemF32>, grid, block, sh, st, pdl, p);
     case kPathSmemBf16:
-      select_shared_kernel<kPathSmemBf16><<<grid, block, sh, st>>>(p);
-      break;
+      return launch_pdl(select_shared_kernel<kPathSmemBf16>, grid, block, sh, st, pdl, p);
     case kPathSmemGroup:
-      select_shared_kernel<kPathSmemGroup><<<grid, block, sh, st>>>(p);
-      break;
+      return launch_pdl(select_shared_kernel<kPathSmemGroup>, grid, block, sh, st, pdl, p);
     default:
       return cudaErrorInvalidValue;
   }
-  return cudaGetLastError();
 }
 
 int select_shared_blocks_per_sm(int path, int block, size_t smem) {
