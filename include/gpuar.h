@@ -76,7 +76,11 @@ int gpuar_destroy(gpuar_t h);
 /* Enqueue all later work on `stream` (a cudaStream_t of the handle's device, passed as
  * void* so this header does not need the CUDA headers).  The new stream is ordered after
  * the work already queued on the previous one (event wait): a handle's launches share its
- * device scratch and must never overlap.  Use one handle per concurrent stream. */
+ * device scratch and must never overlap.  Use one handle per concurrent stream.
+ * Kernels are launched with programmatic dependent launch (an early-scheduled grid waits in
+ * its first instruction until every earlier grid of the stream has completed), so stream
+ * order is exactly that of plain launches; GPUAR_NO_PDL=1 in the environment at
+ * gpuar_create turns the attribute off. */
 int gpuar_set_stream(gpuar_t h, void *stream);
 
 /* Register the propensities (device pointer, binary32, BORROWED).

@@ -251,7 +251,7 @@ int launch_select(gpuar_handle* h, const float* alpha, int64_t rows, int64_t ld,
     p.log2_block = (uint32_t)h->rows_lb;
     const int64_t per_cta = (int64_t)h->rows_warps << h->rows_lb;
     const int grid = (int)std::min<int64_t>(h->rows_grid, (K + per_cta - 1) / per_cta);
-    e = launch_select_rows(p, std::max(grid, 1), h->rows_warps, st);
+    e = launch_select_rows(p, std::max(grid, 1), h->rows_warps, st, h->pdl);
   }
   return cuda_status(e);
 }
@@ -275,10 +275,10 @@ int register_shared(gpuar_handle* h, const float* d_alpha) {
     if (a != cudaSuccess) return cuda_status(a);
   }
   cudaError_t e = launch_stats(d_alpha, (uint32_t)h->M, h->d_part_sum, h->d_part_max, h->d_stats, h->d_ctr,
-                               h->stats_blocks, h->stream);
+                               h->stats_blocks, h->stream, h->pdl);
   if (e == cudaSuccess)
     e = launch_thresholds(d_alpha, (uint32_t)h->M, h->d_stats, h->d_thr, h->d_pref, h->n_pref, h->group_shift,
-                          h->shared_path, h->stream);
+                          h->shared_path, h->stream, h->pdl);
   if (e != cudaSuccess) return cuda_status(e);
   h->alpha = d_alpha;
   h->rows = 1;
@@ -734,7 +734,7 @@ int gpuar_row_stats(gpuar_t h, float* d_amax, double* d_a0) {
   p.log2_block = (uint32_t)h->rows_lb;
   const int64_t per_cta = (int64_t)h->rows_warps << h->rows_lb;
   const int grid = (int)std::min<int64_t>(h->rows_grid, (h->rows + per_cta - 1) / per_cta);
-  return cuda_status(launch_select_rows(p, std::max(grid, 1), h->rows_warps, h->stream));
+  return cuda_status(launch_select_rows(p, std::max(grid, 1), h->rows_warps, h->stream, h->pdl));
 }
 
 int gpuar_sync(gpuar_t h) {

@@ -368,9 +368,9 @@ cudaError_t launch_pdl(void (*kernel)(KArgs...), int grid, int block, size_t sme
 // ---------------------------------------------------------------- launchers (host)
 
 cudaError_t launch_stats(const float* alpha, uint32_t M, double* part_sum, uint32_t* part_max,
-                         DevStats* stats, DevCounters* ctr, int stats_blocks, cudaStream_t st);
+                         DevStats* stats, DevCounters* ctr, int stats_blocks, cudaStream_t st, bool pdl);
 cudaError_t launch_thresholds(const float* alpha, uint32_t M, const DevStats* stats, uint32_t* thr, uint16_t* pref,
-                              uint32_t n_pref, uint32_t group_shift, int path, cudaStream_t st);
+                              uint32_t n_pref, uint32_t group_shift, int path, cudaStream_t st, bool pdl);
 cudaError_t launch_select_shared(const SharedParams& p, int path, int grid, int block, cudaStream_t st, bool pdl);
 cudaError_t launch_argmin_shared(const SharedParams& p, bool smem, int grid, int block, cudaStream_t st, bool pdl);
 void set_argmin_limits(int bytes);
@@ -380,7 +380,7 @@ void set_it_limits(int bytes);
 cudaError_t launch_ssa(const SsaParams& p, int grid, int warps, cudaStream_t st);
 int ssa_blocks_per_sm(int warps, size_t smem);
 void set_ssa_limits(int bytes);
-cudaError_t launch_select_rows(const RowsParams& p, int grid, int warps, cudaStream_t st);
+cudaError_t launch_select_rows(const RowsParams& p, int grid, int warps, cudaStream_t st, bool pdl);
 cudaError_t launch_histogram(const int32_t* idx, const uint32_t* trials, uint32_t K, uint32_t M,
                              unsigned long long* hist, unsigned long long* totals, int grid,
                              cudaStream_t st);

@@ -46,6 +46,8 @@ __global__ void __launch_bounds__(kStatsThreads) stats_pass1(const float* __rest
                                                              double* part_sum, uint32_t* part_max) {
   __shared__ double sh_sum[kStatsThreads / 32];
   __shared__ uint32_t sh_max[kStatsThreads / 32];
+  pdl_wait();  // programmatic dependent launch (gpuar_internal.cuh)
+  pdl_launch_dependents();
   const uint32_t chunk = (M + gridDim.x - 1) / gridDim.x;
   const uint32_t lo = blockIdx.x * chunk;
   const uint32_t hi = min(M, lo + chunk);
@@ -68,6 +70,8 @@ __global__ void __launch_bounds__(kStatsThreads) stats_pass2(const double* part_
                                                              DevCounters* ctr) {
   __shared__ double sh_sum[kStatsThreads / 32];
   __shared__ uint32_t sh_max[kStatsThreads / 32];
+  pdl_wait();
+  pdl_launch_dependents();
   double acc = 0.0;
   uint32_t mx = 0;
   for (int i = threadIdx.x; i < nparts; i += kStatsThreads) {
@@ -122,6 +126,8 @@ __device__ __forceinline__ uint32_t accept_threshold(float alpha_j, float amax) 
 //          (x >> 16) > G_g rejects every j of the group; otherwise the exact T_j decides.
 __global__ void thresholds_kernel(const float* __restrict__ alpha, uint32_t M, const DevStats* __restrict__ stats,
                                   uint32_t* thr, uint16_t* pref, uint32_t n_pref, uint32_t group_shift, int path) {
+  pdl_wait();
+  pdl_launch_dependents();
   const DevStats st = *stats;
   if (!st.valid) return;  // the select kernels stop on invalid statistics
   const float amax = __uint_as_float(st.amax_bits);
@@ -199,19 +205,20 @@ __global__ void __launch_bounds__(256) bench_philox_kernel(uint32_t n_threads, u
 }  // namespace
 
 cudaError_t launch_stats(const float* alpha, uint32_t M, double* part_sum, uint32_t* part_max, DevStats* stats,
-                         DevCounters* ctr, int stats_blocks, cudaStream_t st) {
-  stats_pass1<<<stats_blocks, kStatsThreads, 0, st>>>(alpha, M, part_sum, part_max);
-  stats_pass2<<<1, kStatsThreads, 0, st>>>(part_sum, part_max, stats_blocks, M, stats, ctr);
-  return cudaGetLastError();
+                         DevCounters* ctr, int stats_blocks, cudaStream_t st, bool pdl) {
+  cudaError_t e = launch_pdl(stats_pass1, stats_blocks, kStatsThreads, 0, st, pdl, alpha, M, part_sum, part_max);
+  if (e == cudaSuccess)
+    e = launch_pdl(stats_pass2, 1, kStatsThreads, 0, st, pdl, (const double*)part_sum, (const uint32_t*)part_max,
+                   stats_blocks, M, stats, ctr);
+  return e;
 }
 
 cudaError_t launch_thresholds(const float* alpha, uint32_t M, const DevStats* stats, uint32_t* thr, uint16_t* pref,
-                              uint32_t n_pref, uint32_t group_shift, int path, cudaStream_t st) {
+                              uint32_t n_pref, uint32_t group_shift, int path, cudaStream_t st, bool pdl) {
   const int block = 256;
   const uint32_t n = path == kPathSmemGroup ? n_pref : M;
   const int grid = (int)std::min<uint32_t>((n + block - 1) / block, 4096u);
-  thresholds_kernel<<<grid, block, 0, st>>>(alpha, M, stats, thr, pref, n_pref, group_shift, path);
-  return cudaGetLastError();
+  return launch_pdl(thresholds_kernel, grid, block, 0, st, pdl, alpha, M, stats, thr, pref, n_pref, group_shift, path);
 }
 
 cudaError_t launch_histogram(const int32_t* idx, const uint32_t* trials, uint32_t K, uint32_t M,

@@ -128,6 +128,8 @@ constexpr int kModeStats = 2;
 template <int MAXW, int MODE>
 __global__ void __launch_bounds__(MAXW * 32, 1) select_rows_kernel(const RowsParams P) {
   extern __shared__ __align__(128) unsigned char smem[];
+  pdl_wait();  // programmatic dependent launch: the rows may come from the previous grid
+  pdl_launch_dependents();
   const uint32_t warps = blockDim.x >> 5;
   const uint32_t warp = threadIdx.x >> 5;
   const uint32_t lane = threadIdx.x & 31u;
@@ -290,14 +292,10 @@ __global__ void __launch_bounds__(MAXW * 32, 1) select_rows_kernel(const RowsPar
 }
 
 template <int MAXW>
-cudaError_t launch_w(const RowsParams& p, int grid, int warps, size_t sh, cudaStream_t st) {
-  if (p.stats_only)
-    select_rows_kernel<MAXW, kModeStats><<<grid, warps * 32, sh, st>>>(p);
-  else if (p.rule == kRuleArgmin)
-    select_rows_kernel<MAXW, kRuleArgmin><<<grid, warps * 32, sh, st>>>(p);
-  else
-    select_rows_kernel<MAXW, kRuleClassic><<<grid, warps * 32, sh, st>>>(p);
-  return cudaGetLastError();
+cudaError_t launch_w(const RowsParams& p, int grid, int warps, size_t sh, cudaStream_t st, bool pdl) {
+  if (p.stats_only) return launch_pdl(select_rows_kernel<MAXW, kModeStats>, grid, warps * 32, sh, st, pdl, p);
+  if (p.rule == kRuleArgmin) return launch_pdl(select_rows_kernel<MAXW, kRuleArgmin>, grid, warps * 32, sh, st, pdl, p);
+  return launch_pdl(select_rows_kernel<MAXW, kRuleClassic>, grid, warps * 32, sh, st, pdl, p);
 }
 
 template <int MAXW>
@@ -309,13 +307,13 @@ void set_limits_w(int bytes) {
 
 }  // namespace
 
-cudaError_t launch_select_rows(const RowsParams& p, int grid, int warps, cudaStream_t st) {
+cudaError_t launch_select_rows(const RowsParams& p, int grid, int warps, cudaStream_t st, bool pdl) {
   const size_t S = (size_t)1 << p.log2_stages;
   const size_t sh = (((size_t)warps * S * 8u + 127u) & ~(size_t)127u) + (size_t)warps * S * p.stage_bytes;
-  if (warps <= 16) return launch_w<16>(p, grid, warps, sh, st);
-  if (warps <= 20) return launch_w<20>(p, grid, warps, sh, st);
-  if (warps <= 24) return launch_w<24>(p, grid, warps, sh, st);
-  return launch_w<32>(p, grid, warps, sh, st);
+  if (warps <= 16) return launch_w<16>(p, grid, warps, sh, st, pdl);
+  if (warps <= 20) return launch_w<20>(p, grid, warps, sh, st, pdl);
+  if (warps <= 24) return launch_w<24>(p, grid, warps, sh, st, pdl);
+  return launch_w<32>(p, grid, warps, sh, st, pdl);
 }
 
 int select_rows_blocks_per_sm(int warps, size_t smem) {
