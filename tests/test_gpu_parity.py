@@ -174,6 +174,19 @@ def test_max_trials_rejected_path(mt):
     assert (out[0].cpu() == -1).any()
 
 
+@pytest.mark.parametrize("mt", [300, 1001, 1 << 20])
+def test_long_selections_few_per_warp(mt):
+    # whole-warp teams with few selections per warp and ~E = 844 trials each (many rounds
+    # per selection, the launch's tail made of long selections), including selections
+    # rejected at a max_trials cap that is not a multiple of a round's 64 trials
+    a = synth.pareto(100_000)
+    sel, out, ref = _shared_case(a, 3000, max_trials=mt, epoch=2, s0=99)
+    assert sel.last_team == 32
+    _check(out, ref)
+    if mt < 2000:
+        assert (out[0].cpu() == -1).any()
+
+
 def test_epochs_offsets_and_replay():
     a = synth.exponential(1000)
     sel = _sel(a.size, 5000)
