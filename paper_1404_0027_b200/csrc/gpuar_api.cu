@@ -325,7 +325,8 @@ int gpuar_create(gpuar_t* out, int64_t M, int64_t K, uint64_t seed) {
   {
     const size_t am_sh = (size_t)((M + 3) & ~3ll) * 8u;  // alpha and RN(1/alpha) in smem
     h->am_smem = am_sh + 1024u <= (size_t)h->smem_optin;
-    h->am_grid = h->num_sms * 8;  // 8 x 256 threads per SM (occupancy-capped by the runtime)
+    // one resident wave of 256-thread CTAs (the selections are assigned statically per warp)
+    h->am_grid = h->num_sms * std::max(1, argmin_blocks_per_sm(h->am_smem, h->am_smem ? am_sh : 0));
   }
   // stats launch shape depends on M only -> identical reduction tree on every rank
   h->stats_blocks = (int)std::min<int64_t>((M + 4095) / 4096, 512);

@@ -374,6 +374,7 @@ cudaError_t launch_thresholds(const float* alpha, uint32_t M, const DevStats* st
 cudaError_t launch_select_shared(const SharedParams& p, int path, int grid, int block, cudaStream_t st, bool pdl);
 cudaError_t launch_argmin_shared(const SharedParams& p, bool smem, int grid, int block, cudaStream_t st, bool pdl);
 void set_argmin_limits(int bytes);
+int argmin_blocks_per_sm(bool smem, size_t bytes);
 cudaError_t launch_it_prefix(const float* alpha, uint32_t M, double* C, cudaStream_t st);
 cudaError_t launch_it_select(const SharedParams& p, const double* C, bool smem, int grid, cudaStream_t st, bool pdl);
 void set_it_limits(int bytes);

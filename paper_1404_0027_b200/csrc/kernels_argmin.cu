@@ -170,6 +170,14 @@ cudaError_t launch_argmin_shared(const SharedParams& p, bool smem, int grid, int
   return launch_pdl(argmin_shared_kernel<false>, grid, block, 0, st, pdl, p);
 }
 
+int argmin_blocks_per_sm(bool smem, size_t bytes) {
+  int n = 0;
+  const cudaError_t e =
+      smem ? cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, argmin_shared_kernel<true>, 256, bytes)
+           : cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, argmin_shared_kernel<false>, 256, 0);
+  return e == cudaSuccess ? n : 0;
+}
+
 void set_argmin_limits(int bytes) {
   set_max_dynamic_smem(argmin_shared_kernel<true>, bytes);
 }
