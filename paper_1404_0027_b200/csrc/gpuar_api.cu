@@ -225,6 +225,18 @@ int launch_select(gpuar_handle* h, const float* alpha, int64_t rows, int64_t ld,
       if (e == cudaSuccess) e = launch_it_select(p, h->d_prefix, smem, h->num_sms * 8, st, h->pdl);
     } else {
       p.phase = h->ticket_phase;
+      {
+        const uint64_t nwarps = (uint64_t)h->sh_grid * (uint64_t)h->sh_block / 32u;
+        const uint64_t fair = std::max<uint64_t>(1u, (uint64_t)K / nwarps);
+        uint64_t first = fair / 2u;
+        if (fair <= 4u) {
+          const uint64_t stripe = ((uint64_t)K + kStripes - 1u) / kStripes;
+          const uint64_t per = std::max<uint64_t>(1u, nwarps / kStripes);  // fewest warps any stripe has
+          first = (stripe + per - 1u) / per;
+        }
+        p.fair = (uint32_t)fair;
+        p.first_base = (uint32_t)first;
+      }
       e = launch_select_shared(p, h->shared_path, h->sh_grid, h->sh_block, st, h->pdl);
       if (e == cudaSuccess) h->ticket_phase ^= 1u;
     }

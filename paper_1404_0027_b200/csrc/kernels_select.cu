@@ -390,16 +390,11 @@ __global__ void __launch_bounds__(1024, 1) select_shared_kernel(const SharedPara
   // static first chunk: half of a warp's fair share; then grabs of ~8192 expected trials
   // (st.grab), at most an eighth of the fair share (but two teams' worth), at least one
   // selection per team; tickets are prefetched one chunk ahead.
+  // (fair = max(1, K / warps) and the static chunk come from the host, launch_select: two
+  // 64-bit divisions per warp were ~100 of the ~170 set-up instructions of every warp)
   const unsigned long long teams = 32u / g;
-  const unsigned long long fair = max(1ull, (unsigned long long)K / nwarps);
-  unsigned long long first = max(teams, fair / 2ull);
-  if (fair <= 4ull) {
-    // a few selections per warp: static chunks that cover each stripe, no tickets at all
-    // (the atomic's round trip would cost more than any imbalance it evens out)
-    const unsigned long long stripe = ((unsigned long long)K + kStripes - 1) / kStripes;
-    const unsigned long long per = max(1u, nwarps / kStripes);  // fewest warps any stripe has
-    first = max(teams, (stripe + per - 1) / per);
-  }
+  const unsigned long long fair = P.fair;
+  const unsigned long long first = max(teams, (unsigned long long)P.first_base);
   // (r01 sweep, GPUAR_GRAB: c2 best at 2 with prefetch; heavy tails (st.grab = 1) at 1)
   unsigned long long grab = max(teams, min((unsigned long long)st.grab, max(2ull * teams, fair / 8ull)));
   if (P.grab_override) grab = P.grab_override;
