@@ -210,7 +210,7 @@ __device__ __forceinline__ void trial_loop(const SharedParams& P, const TrialStr
 // rounds finish some lane, so the hand-out has a fast path: the current chunk covers every
 // idle lane -> one popc and a 32-bit add (selection indices are < K < 2^32); only a chunk
 // boundary takes the general loop (refill / prefetch).
-template <int PATH>
+template <int PATH, int NC>
 __device__ __forceinline__ void lane_loop(const SharedParams& P, const TrialStream& ts, uint32_t sbase, Pool pl) {
   const uint32_t M = P.M;
   const uint32_t half = P.max_trials >> 1;
@@ -254,6 +254,9 @@ __device__ __forceinline__ void lane_loop(const SharedParams& P, const TrialStre
         if (pl.exhausted && !__any_sync(kFull, active)) break;
       }
     }
+    // NC = 1: call c (trials 2c, 2c+1); NC = 2: calls c and c+1 (trials 2c .. 2c+3), decided
+    // in canonical order -- half the per-round bookkeeping per call at the price of the
+    // second call when the first accepts (used for p <= 1/4, kernel dispatch below)
     const Philox4 x = ts(c, sel);
     const uint32_t j0 = __umulhi(x.x, M);
     const uint32_t j1 = __umulhi(x.z, M);
@@ -261,13 +264,23 @@ __device__ __forceinline__ void lane_loop(const SharedParams& P, const TrialStre
     const bool r1 = accept<PATH>(x.w, j1, sbase, P.thr, P.group_shift);
     const bool a0 = (c < calls) & r0;
     const bool a1 = (c < half) & r1;
-    const bool done = active & (a0 | a1 | (c + 1u >= calls));
+    bool a2 = false, a3 = false;
+    uint32_t j2 = 0, j3 = 0;
+    if constexpr (NC == 2) {
+      const Philox4 y = ts(c + 1u, sel);
+      j2 = __umulhi(y.x, M);
+      j3 = __umulhi(y.z, M);
+      a2 = (c + 1u < calls) & accept<PATH>(y.y, j2, sbase, P.thr, P.group_shift);
+      a3 = (c + 1u < half) & accept<PATH>(y.w, j3, sbase, P.thr, P.group_shift);
+    }
+    const bool done = active & (a0 | a1 | a2 | a3 | (c + (uint32_t)NC >= calls));
     if (done) {
-      idx_out[my] = a0 ? (int32_t)j0 : (a1 ? (int32_t)j1 : -1);
-      if (want_tr) tr_out[my] = a0 ? 2u * c + 1u : (a1 ? 2u * c + 2u : P.max_trials);
+      idx_out[my] = a0 ? (int32_t)j0 : a1 ? (int32_t)j1 : a2 ? (int32_t)j2 : a3 ? (int32_t)j3 : -1;
+      if (want_tr)
+        tr_out[my] = a0 ? 2u * c + 1u : a1 ? 2u * c + 2u : a2 ? 2u * c + 3u : a3 ? 2u * c + 4u : P.max_trials;
       active = false;
     }
-    ++c;
+    c += NC;
     need = __ballot_sync(kFull, !active);
   }
 }
@@ -314,7 +327,8 @@ __device__ __forceinline__ void warp_loop(const SharedParams& P, const TrialStre
 // Team size g (power of two, 1..32) minimising the estimated warp instructions per
 // selection (E = 1/p expected trials; SASS counts of the r01 build):
 //   g = 32 (warp_loop): (E/64 + 1/2) rounds x 62 + 15 per selection;
-//   g = 1 (lane_loop): (E + 1)/64 warp-rounds x (72 + 45 P(any lane of the warp finished));
+//   g = 1 (lane_loop): (E + 1)/64 warp-rounds x (72 + 45 P(any lane of the warp finished)),
+//     or with two calls per round (1/128 <= p <= 1/4) (E + 2)/128 warp-rounds x (117 + 45 P(any));
 //   1 < g < 32 (trial_loop): (E + g)/64 warp-rounds x (67 + 45 P(any lane finished));
 // (finish costs recalibrated in session 2: ncu counts ~125 warp instructions per lane-loop
 // round when a lane finishes almost every round (c3 exponential, M = 10^4), and the
@@ -329,10 +343,23 @@ __device__ __forceinline__ uint32_t choose_team(float p, uint32_t K, uint32_t nw
   uint32_t best = 32u;
   float best_cost = (E / 64.0f + 0.5f) * 62.0f + 15.0f;
   best_cost *= 1.0f + 0.06931f * wk;
+  // lane loop with two calls per round (p <= 1/4): 128 trials per warp-round at ~117
+  // instructions plus the finish handling.  Considered only up to E = 128: measured +16-20 %
+  // at E = 14 and 73 (c3 exponential M = 10^5, Pareto M = 10^3) but -29 % at E = 292 and
+  // -31 % at E ~ 10^5 (c3 Pareto M = 10^4, c5), where the last selection of each lane
+  // leaves most of the warp idle (the drain term above underrates that tail)
+  const float any2 = 1.0f - __expf(128.0f * __logf(fmaxf(1.0f - p, 1e-30f)));
   for (uint32_t g = 1u; g < 32u; g <<= 1) {
     const float T = (float)(32u / g);
-    const float round = (g == 1u) ? 72.0f + 45.0f * any : 67.0f + 45.0f * any;
-    const float cost = (E + (float)g) / 64.0f * round * (1.0f + 0.1f * T * __logf(T + 1.0f) * wk);
+    float rounds, round;
+    if (g == 1u && p <= 0.25f && p >= 1.0f / 128.0f) {
+      rounds = (E + 2.0f) / 128.0f;
+      round = 117.0f + 45.0f * any2;
+    } else {
+      rounds = (E + (float)g) / 64.0f;
+      round = (g == 1u) ? 72.0f + 45.0f * any : 67.0f + 45.0f * any;
+    }
+    const float cost = rounds * round * (1.0f + 0.1f * T * __logf(T + 1.0f) * wk);
     if (cost < best_cost) {
       best_cost = cost;
       best = g;
@@ -401,8 +428,12 @@ __global__ void __launch_bounds__(1024, 1) select_shared_kernel(const SharedPara
   Pool pl;
   pool_init(pl, K, nwarps, warp_global, first, grab, P.ctr->next[P.phase], P.no_prefetch == 0u);
   const TrialStream ts(P.seed_lo, P.seed_hi, P.epoch);
-  if (g == 1u)
-    lane_loop<PATH>(P, ts, sbase, pl);
+  if (g == 1u) {
+    if (st.p <= 0.25f)
+      lane_loop<PATH, 2>(P, ts, sbase, pl);
+    else
+      lane_loop<PATH, 1>(P, ts, sbase, pl);
+  }
   else if (g == 32u)
     warp_loop<PATH>(P, ts, sbase, pl);
   else

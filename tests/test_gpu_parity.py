@@ -174,6 +174,16 @@ def test_max_trials_rejected_path(mt):
     assert (out[0].cpu() == -1).any()
 
 
+@pytest.mark.parametrize("mt", [1, 2, 3, 4, 5, 7, 1 << 20])
+def test_lane_teams_two_calls_per_round_caps(mt):
+    # one lane per selection with two Philox calls per round (p <= 1/4): max_trials caps
+    # that end inside the round's first or second call, on either word
+    a = synth.exponential(1000)
+    sel, out, ref = _shared_case(a, 1 << 18, max_trials=mt, epoch=5, s0=12345)
+    assert sel.last_team == 1
+    _check(out, ref)
+
+
 @pytest.mark.parametrize("mt", [300, 1001, 1 << 20])
 def test_long_selections_few_per_warp(mt):
     # whole-warp teams with few selections per warp and ~E = 844 trials each (many rounds
