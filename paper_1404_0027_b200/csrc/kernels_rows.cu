@@ -93,9 +93,21 @@ __device__ __forceinline__ void rate_calls(const Philox4 (&x)[N], const uint32_t
 
 // The paper's printed rule on one row (R16-R19): lane l rates reactions 4c..4c+3
 // of its calls c = l, l+32, ...; warp butterfly on the (rating bits, index) key.
+// Leftover calls precomputed for a batch of rows (see the kernel): when every lane runs the
+// same number of pair iterations and 1 or 2 calls are left per row, the Philox words of the
+// leftovers of the next kLeftRows rows are drawn in one warp-wide step (lane l: row
+// l / L, call 64 nP + l % L) and each row takes its words by shuffle -- one Philox latency
+// per 16 rows instead of per row.
+constexpr uint32_t kLeftRows = 16;
+struct Leftover {
+  bool batched;    // the batched path applies to this launch's M
+  uint32_t src;    // lane holding this row's first leftover call
+  Philox4 x;       // this lane's precomputed words
+};
+
 template <bool FOLD, class Stream>
 __device__ __forceinline__ void row_argmin(const Stream& ts, uint32_t sel, uint32_t row_s, uint32_t M, float T,
-                                           uint32_t lane, int32_t& id) {
+                                           uint32_t lane, int32_t& id, const Leftover& lo) {
   const float T_s = __fmul_rn(T, 0x1p-24f);
   const uint32_t k1t = ts.rk1[0] ^ kTagElection;
   const uint32_t full = M >> 2;  // calls whose four reactions all exist
@@ -109,12 +121,25 @@ __device__ __forceinline__ void row_argmin(const Stream& ts, uint32_t sel, uint3
     const uint32_t cc[2] = {c, c + 32u};
     rate_calls<2, FOLD, true>(x, cc, row_s, M, T, T_s, bestR, bestJ);
   }
-  // the leftover calls (at most two per lane; at M = 1029 lane 0 has call 256 and lane 1
-  // the partial call 257) in ONE predicated step, so the warp pays one Philox latency
-  for (; c < calls; c += 32u) {
-    const Philox4 x[1] = {ts.with_tag(c, sel, k1t)};
-    const uint32_t cc[1] = {c};
-    rate_calls<1, FOLD, false>(x, cc, row_s, M, T, T_s, bestR, bestJ);
+  if (lo.batched) {  // c = lane + 64 nP for every lane; lanes < L rate their call
+    Philox4 xb;
+    xb.x = __shfl_sync(kFull, lo.x.x, lo.src + lane);
+    xb.y = __shfl_sync(kFull, lo.x.y, lo.src + lane);
+    xb.z = __shfl_sync(kFull, lo.x.z, lo.src + lane);
+    xb.w = __shfl_sync(kFull, lo.x.w, lo.src + lane);
+    if (c < calls) {
+      const Philox4 x[1] = {xb};
+      const uint32_t cc[1] = {c};
+      rate_calls<1, FOLD, false>(x, cc, row_s, M, T, T_s, bestR, bestJ);
+    }
+  } else {
+    // the leftover calls (at most two per lane) in ONE predicated step, so the warp pays
+    // one Philox latency
+    for (; c < calls; c += 32u) {
+      const Philox4 x[1] = {ts.with_tag(c, sel, k1t)};
+      const uint32_t cc[1] = {c};
+      rate_calls<1, FOLD, false>(x, cc, row_s, M, T, T_s, bestR, bestJ);
+    }
   }
   unsigned long long best = ((unsigned long long)__float_as_uint(bestR) << 32) | bestJ;
 #pragma unroll
@@ -193,6 +218,14 @@ __global__ void __launch_bounds__(MAXW * 32, 1) select_rows_kernel(const RowsPar
   const uint32_t half = P.max_trials >> 1;
   const uint32_t calls = half + (P.max_trials & 1u);
   const TrialStream ts(P.seed_lo, P.seed_hi, P.epoch);
+  // argmin rule: batched leftover calls when every lane runs floor(full / 64) pair
+  // iterations ((full mod 64) <= 32) and 1 or 2 calls remain (M = 1029: calls 256, 257)
+  const uint32_t full4 = M >> 2, ncalls4 = (M + 3u) >> 2;
+  const uint32_t left_c0 = full4 & ~63u, nleft = ncalls4 - left_c0;
+  Leftover left;
+  left.batched = MODE == kRuleArgmin && (full4 & 63u) <= 32u && nleft >= 1u && nleft <= 2u;
+  left.src = 0;
+  left.x = Philox4{0u, 0u, 0u, 0u};
   float nlog = 0.f;  // -ln(u1) of row_of(n0 + lane)
   // this lane's buffered outputs for row (block base + lane); tau is formed at the flush,
   // one division per block: tau = -ln(u1) / fl32(alpha_0), with fl32(alpha_0) = 0 for an
@@ -209,6 +242,14 @@ __global__ void __launch_bounds__(MAXW * 32, 1) select_rows_kernel(const RowsPar
     if ((n & 31u) == 0u && MODE != kModeStats) {
       const uint32_t nn = n + lane;
       nlog = nn < n_rows ? neg_log_u1(P.seed_lo, P.seed_hi, P.s0 + row_of(nn), P.epoch) : 0.f;
+    }
+    if constexpr (MODE == kRuleArgmin) {
+      if (left.batched && (n & (kLeftRows - 1u)) == 0u) {  // leftovers of rows n .. n+15
+        const uint32_t nn = n + lane / nleft;
+        if (lane < kLeftRows * nleft && nn < n_rows)
+          left.x = ts.with_tag(left_c0 + lane % nleft, ts.sel_word(P.s0 + row_of(nn)), ts.rk1[0] ^ kTagElection);
+      }
+      left.src = (n & (kLeftRows - 1u)) * nleft;
     }
     mbar_wait_s(bars_s + 8u * slot, parity);
     // The slot holds the row's 16-byte hull: element j sits at word lead + j.
@@ -243,9 +284,9 @@ __global__ void __launch_bounds__(MAXW * 32, 1) select_rows_kernel(const RowsPar
           // the paper's printed rule on this row: election + argmin selection
           const float T = __fmul_rn(P.w, amax);
           if (can_fold(__float_as_uint(T)))
-            row_argmin<true>(ts, sel, row_s, M, T, lane, id);
+            row_argmin<true>(ts, sel, row_s, M, T, lane, id, left);
           else
-            row_argmin<false>(ts, sel, row_s, M, T, lane, id);
+            row_argmin<false>(ts, sel, row_s, M, T, lane, id, left);
           tr = M;
         } else {
           // (two Philox calls per lane per round -- 128 trials -- measured +7 % instructions
