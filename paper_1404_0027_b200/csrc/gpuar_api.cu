@@ -145,16 +145,27 @@ void plan_shared(gpuar_handle* h) {
     h->n_pref = (uint32_t)((M + (1ull << s) - 1) >> s);
     h->shared_smem = (uint32_t)(((2u * h->n_pref + 15u) & ~15ull) + 16u);
   }
-  // block size maximising resident threads per SM (GPUAR_SH_CTAS_PER_SM: fewer CTAs, tuning)
-  int best_threads = 0;
+  // CTA size: the largest block whose resident threads per SM reach 3/4 of the best any size
+  // gets.  Fewer, larger CTAs amortise the per-CTA set-up (staging, statistics, team choice,
+  // barrier): 1 x 1024 threads beat 5 x 256 (the occupancy maximum at 48 registers) on every
+  // smem-vector config, +4-7 % (session-2 sweep, GPUAR_SH_BLOCK).  GPUAR_SH_CTAS_PER_SM caps
+  // the CTAs per SM, GPUAR_SH_BLOCK forces a size (tuning).
   const int cap = env_int("GPUAR_SH_CTAS_PER_SM", 0);
-  for (int block : {256, 512, 1024}) {
-    int n = select_shared_blocks_per_sm(h->shared_path, block, h->shared_smem);
+  const int force_block = env_int("GPUAR_SH_BLOCK", 0);
+  int nb[3] = {0, 0, 0}, best_threads = 0;
+  const int blocks[3] = {256, 512, 1024};
+  for (int i = 0; i < 3; ++i) {
+    if (force_block > 0 && blocks[i] != force_block) continue;
+    int n = select_shared_blocks_per_sm(h->shared_path, blocks[i], h->shared_smem);
     if (cap > 0) n = std::min(n, cap);
-    if (n * block > best_threads) {
-      best_threads = n * block;
-      h->sh_block = block;
-      h->sh_grid = n * h->num_sms;
+    nb[i] = n;
+    best_threads = std::max(best_threads, n * blocks[i]);
+  }
+  for (int i = 2; i >= 0; --i) {
+    if (nb[i] > 0 && 4 * nb[i] * blocks[i] >= 3 * best_threads) {
+      h->sh_block = blocks[i];
+      h->sh_grid = nb[i] * h->num_sms;
+      break;
     }
   }
 }
