@@ -204,8 +204,8 @@ __device__ __forceinline__ void trial_loop(const SharedParams& P, const TrialStr
   }
 }
 
-// One lane per selection (g = 1, high p): every round each lane makes one Philox call for
-// its own selection; a lane that finishes stores its result and takes the next selection of
+// One lane per selection (g = 1, high p): every round each lane makes NC Philox calls (1, or
+// 2 for p <= 1/4) for its own selection; a lane that finishes stores its result and takes the next selection of
 // the warp's pool (one ballot + popc), with no cross-lane data exchange.  At high p most
 // rounds finish some lane, so the hand-out has a fast path: the current chunk covers every
 // idle lane -> one popc and a 32-bit add (selection indices are < K < 2^32); only a chunk
