@@ -2,13 +2,21 @@
 """bench.py -- GPU-AR next-reaction selections/sec on B200 (BASELINE.json metric).
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--config c4] [--impl gpuar|reference]
+                    [--scaling weak|strong]
 
 One JSON line on rank 0.  Default workload (config c4, the per-realization K x M matrix
 named by BASELINE.json for 1/2/4/8 B200): M = 1029 yeast-like reactions, K = 2^20
 realizations PER GPU (weak scaling: each rank owns global rows [r*K, (r+1)*K), generated in
-its own HBM by libsynth -- no data-path collective).  A step is one gpuar_select over the
-K resident rows: per-row alpha_max / alpha_0 reductions, AR trials, tau (one kernel).
-The 4.3 GB matrix is > L2 (126 MB), so no L2 flush is needed between steps.
+its own HBM by libsynth -- no data-path collective); --scaling strong splits K = 2^20 in
+total over the ranks, and an N > 1 weak run also reports that strong
+split as a sub-record.  A step is one gpuar_select over the K resident rows: per-row
+alpha_max / alpha_0 reductions, AR trials, tau (one kernel).  The 4.3 GB matrix is > L2
+(126 MB), so no L2 flush is needed between steps.
+
+--gpus N without a torch.distributed launcher (no WORLD_SIZE in the environment) re-runs
+this script under `python -m torch.distributed.run --nproc-per-node N` itself, one rank per
+GPU; fewer than N visible GPUs is an error (--oversubscribe allows ranks to share GPUs over
+gloo, for dry runs and tests only, and says so in the JSON line).
 
 --impl reference times the CPU oracle (oracle/, the parity reference) on rank 0 on a
 bounded sample of the same workload per step; the other ranks exit 0.
@@ -52,7 +60,11 @@ CONFIGS = {
                desc="c3: shared simulated distribution, K=2^20 selections"),
     "c4": dict(kind="rows", dist="yeast", M=1029, K=1 << 20,
                desc="c4: per-realization KxM matrix, M=1029 yeast-like rows, K=2^20 realizations per GPU"),
-    "c5": dict(kind="shared", dist="pareto", M=1_000_000, K=1 << 21,
+    # max_trials 2^24: this seed's Pareto vector has p = 1.03e-5 (E[trials] ~ 9.7e4), so the
+    # default cap 2^20 would reject (1-p)^(2^20) ~ 2e-5 of the selections -- ~340 of 2^24 at
+    # 8 GPUs; at 2^24 P(reject) = e^-173 per selection and the run shows the paper's zero
+    # rejection
+    "c5": dict(kind="shared", dist="pareto", M=1_000_000, K=1 << 21, max_trials=1 << 24,
                desc="c5: M=1e6 Pareto(1.5) shared vector, K=2^21 selections per GPU (2^24 at 8 GPUs)"),
     # NEXT-2: the full SSA loop (propensities + selection + state update) on chip
     "s1": dict(kind="ssa", dist="yeast-network", M=1029, K=1 << 17, inner=16,
@@ -86,6 +98,12 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--dist-backend", default="nccl", help="nccl (default); gloo only to dry-run N ranks on one GPU")
+    ap.add_argument("--scaling", default="weak", choices=["weak", "strong"],
+                    help="weak: K selections per GPU (default); strong: K selections in total, split over the ranks")
+    ap.add_argument("--oversubscribe", action="store_true",
+                    help="allow more ranks than visible GPUs (ranks share GPUs over gloo; dry runs and tests only)")
+    ap.add_argument("--sustain-s", type=float, default=2.0,
+                    help="seconds of the sustained-loop sub-record (0: skip)")
     return ap.parse_args()
 
 
@@ -101,6 +119,9 @@ def workload(args) -> dict:
         w["rule"] = args.rule
     w.setdefault("rule", "classic")
     w["w"] = args.w
+    if args.max_trials:
+        w["max_trials"] = args.max_trials
+    w.setdefault("max_trials", 1 << 20)
     return w
 
 
@@ -190,13 +211,14 @@ def ncu_traffic(config: str):
     return None if e is None else e.get("dram_bytes_per_launch")
 
 
-def make_inputs(w: dict, rank: int, device):
-    """Synthetic, seeded inputs (synth/) already resident in HBM."""
+def make_inputs(w: dict, s0: int, K: int, device):
+    """Synthetic, seeded inputs (synth/) already resident in HBM: the shared vector, or the
+    matrix rows of global selections s0 .. s0+K-1 (each rank generates its own rows)."""
     import numpy as np
     import torch
 
     import synth
-    M, K = w["M"], w["K"]
+    M = w["M"]
     if w["kind"] == "ssa":
         net = synth.yeast_like_network(M=M)
         dev = {k: torch.from_numpy(np.ascontiguousarray(net[k])).to(device) for k in ("reac", "rate", "didx", "dval")}
@@ -207,7 +229,7 @@ def make_inputs(w: dict, rank: int, device):
         import synth.gpu as sg
         rates = torch.from_numpy(synth.yeast_rates(M)).to(device)
         mat = torch.empty((K, M), dtype=torch.float32, device=device)
-        sg.fill_rows(mat, rates, synth.GEN_SEED, rank * K)
+        sg.fill_rows(mat, rates, synth.GEN_SEED, s0)
         return mat
     if w["dist"] == "hand":
         a = synth.hand([1, 2, 3, 4])
@@ -246,7 +268,7 @@ def oracle_pass(w: dict, data, nn: int, epoch: int, threads: int):
     elif w.get("rule") == "it":
         oracle.it_select(alpha, nn, seed=20140327, epoch=epoch, nthreads=threads)
     else:
-        oracle.ar_select(alpha, nn, seed=20140327, epoch=epoch, nthreads=threads)
+        oracle.ar_select(alpha, nn, seed=20140327, epoch=epoch, max_trials=w["max_trials"], nthreads=threads)
     return time.perf_counter() - t0, nn
 
 
@@ -308,36 +330,131 @@ def run_reference(args, w, rank, world):
     out = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": unit_of(w), "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": dt / args.steps * 1e3,
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+        "higher_is_better": True, "scaling": args.scaling, "vs_baseline": None, "dtype": "f32",
         "data": "synthetic", "config": {"workload": w["desc"], "M": w["M"], "K_per_gpu": w["K"]},
-        "cpu_baseline": {"value": value, "unit": unit_of(w), "cores": threads, "kind": "oracle", "sample": sample},
+        "cpu_baseline": {"value": value, "unit": unit_of(w), "cores": threads, "kind": "oracle", "sample": sample,
+                         "cpu_model": cpu_model()},
         "e2e": {"value": value, "unit": unit_of(w), "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(out), flush=True)
 
 
+# ----------------------------------------------------------------- validation (statistics, off the clock)
+
+def chi2_pooled(counts, expected, min_expected: float = 5.0) -> dict:
+    """Pearson chi^2 of observed counts against expected counts, the bins with an expected
+    count < min_expected pooled into one (SURVEY.md §8(c) "law").  Statistics of the
+    outputs only (scipy), not the selection method."""
+    import numpy as np
+    from scipy.stats import chi2
+
+    o = np.asarray(counts, np.float64)
+    e = np.asarray(expected, np.float64)
+    keep = e >= min_expected
+    oo, ee = list(o[keep]), list(e[keep])
+    if (~keep).any():
+        oo.append(o[~keep].sum())
+        ee.append(e[~keep].sum())
+    oo, ee = np.array(oo), np.array(ee)
+    if ((ee == 0) & (oo > 0)).any():
+        return {"stat": float("inf"), "dof": int(oo.size - 1), "p": 0.0, "bins": int(oo.size)}
+    nz = ee > 0
+    stat = float((((oo - ee) ** 2)[nz] / ee[nz]).sum())
+    dof = int(nz.sum() - 1)
+    return {"stat": stat, "dof": dof, "p": float(chi2.sf(stat, dof)) if dof > 0 else 1.0, "bins": int(nz.sum())}
+
+
+def law_and_trials(w: dict, sel, alpha):
+    """(sum over this rank's selections of the exact law alpha_j / alpha_0 as an M-vector,
+    expected sum of trials, its variance) -- float64 CUDA tensors.  Shared vector: one law
+    for every selection; matrix: the row laws summed (chunked, the matrix is 4.3 GB), and
+    E[trials] = 1/p_r, Var = (1 - p_r)/p_r^2 with p_r = alpha_0,r / (M alpha_max,r) from
+    gpuar_row_stats."""
+    import torch
+
+    M = w["M"]
+    if alpha.dim() == 1:
+        a = alpha.double()
+        law = a / a.sum()
+        amax, a0 = a.max(), a.sum()
+        p = a0 / (M * amax)
+        return law, 1.0 / p, (1.0 - p) / (p * p), p
+    amax_r, a0_r = sel.row_stats()
+    law = torch.zeros(M, dtype=torch.float64, device=alpha.device)
+    step = 1 << 16
+    for r in range(0, alpha.shape[0], step):
+        blk = alpha[r:r + step].double()
+        d = a0_r[r:r + step].clone()
+        d[d == 0] = 1.0                       # all-zero rows contribute nothing (and are rejected)
+        law += (blk / d[:, None]).sum(0)
+    ok = amax_r > 0
+    p = a0_r[ok] / (M * amax_r[ok].double())
+    return law, (1.0 / p).sum(), ((1.0 - p) / (p * p)).sum(), None
+
+
 # ----------------------------------------------------------------- our arm
 
+def cpu_model() -> str:
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
 def run_gpuar(args, w, rank, world, local_rank):
+    import numpy as np
     import torch
     import torch.distributed as dist
 
     from paper_1404_0027_b200 import Selector
-    from paper_1404_0027_b200.dist import broadcast_vector, max_over_ranks, reduce_validation, weak_shard
+    from paper_1404_0027_b200.dist import broadcast_vector, max_over_ranks, reduce_validation, shard, weak_shard
 
     device = torch.device("cuda", local_rank)
     torch.cuda.set_device(device)
-    M, K = w["M"], w["K"]
+    M = w["M"]
     seed = 20140327
-    alpha = make_inputs(w, rank, device)
+    # weak: K selections per rank at [r K, (r+1) K); strong: K in total, contiguous shards
+    if args.scaling == "strong":
+        K_total = w["K"]
+        s0, K = shard(K_total, rank, world)
+    else:
+        s0, K = weak_shard(w["K"], rank)
+        K_total = K * world
+    alpha = make_inputs(w, s0, K, device)
     sel = Selector(M, K, seed, device=local_rank)
-    if args.max_trials:
-        sel.set_max_trials(args.max_trials)
+    sel.set_max_trials(w["max_trials"])
     sel.set_rule(w["rule"], w["w"] if w["rule"] == "argmin" else 1.0)
-    s0, _ = weak_shard(K, rank)
     sel.set_selection_offset(s0)
+    stream = torch.cuda.current_stream(device)
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    def ev_pair():
+        return torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+
+    collectives = None
     if w["kind"] == "shared":
-        broadcast_vector(alpha, src=0)          # C1: one shared vector for all ranks
+        if world > 1:
+            # C1: one shared vector for all ranks (warm call, then the timed broadcast)
+            scratch = alpha.clone()
+            broadcast_vector(scratch, src=0)
+            barrier()
+            e0, e1 = ev_pair()
+            e0.record(stream)
+            broadcast_vector(alpha, src=0)
+            e1.record(stream)
+            e1.synchronize()
+            collectives = {"c1_broadcast_ms": max_over_ranks(e0.elapsed_time(e1), device),
+                           "c1_bytes": 4 * M}
+        else:
+            broadcast_vector(alpha, src=0)
     sel.set_propensities(alpha)
     out = (torch.empty(K, dtype=torch.int32, device=device), torch.empty(K, dtype=torch.float32, device=device),
            torch.empty(K, dtype=torch.int32, device=device))
@@ -345,44 +462,107 @@ def run_gpuar(args, w, rank, world, local_rank):
         sel.select(K, out=out)
     sel.sync()
 
-    def barrier():
-        if world > 1:
-            dist.barrier()
-        torch.cuda.synchronize()
+    def timed(n_steps, k=K, o=out):
+        """n_steps consecutive selects between a barrier + synchronize on both sides; CUDA
+        events on the launching stream; (ms of this rank, perf_counter window)."""
+        barrier()
+        t_start = time.perf_counter()
+        e0, e1 = ev_pair()
+        e0.record(stream)
+        for _ in range(n_steps):
+            sel.select(k, out=o)
+        e1.record(stream)
+        e1.synchronize()
+        t_end = time.perf_counter()
+        return e0.elapsed_time(e1), t_start, t_end
 
-    stream = torch.cuda.current_stream(device)
-    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     path = sel.path
     with ClockSampler(local_rank) as clk:
         clk.wait_first()
         for _ in range(max(args.warmup, 3)):      # re-warm after the sampler start-up
             sel.select(K, out=out)
-        barrier()
-        t_start = time.perf_counter()
-        ev0.record(stream)
-        for _ in range(args.steps):
-            sel.select(K, out=out)
-        ev1.record(stream)
-        ev1.synchronize()
-        t_end = time.perf_counter()
+        ms, t_start, t_end = timed(args.steps)
         time.sleep(0.06)
         clk.mark(t_start, t_end)
     barrier()
     sel.sync()
-    ms = ev0.elapsed_time(ev1)
     ms_max = max_over_ranks(ms, device)        # C3
     ms_step = ms_max / args.steps
-    value = K * world * args.steps / (ms_max * 1e-3)
+    value = K_total * args.steps / (ms_max * 1e-3)
+    clocks = clk.summary()
 
-    # validation of the last step (untimed): histogram (+ C2 reduce)
+    # Sustained loop (the paper averages over runs, PAPER.md:657-661): the same step back to
+    # back for >= sustain_s seconds, its own clocks -- the power-capped steady state, next to
+    # the short burst above.
+    sustained = None
+    if args.sustain_s > 0:
+        n_sus = max(args.steps, int(math.ceil(args.sustain_s * 1e3 / max(ms_step, 1e-3))))
+        with ClockSampler(local_rank) as clk2:
+            clk2.wait_first()
+            ms2, ts0, ts1 = timed(n_sus)
+            time.sleep(0.06)
+            clk2.mark(ts0, ts1)
+        ms2_max = max_over_ranks(ms2, device)
+        sus_ms_rank = ms2
+        sustained = {"value": K_total * n_sus / (ms2_max * 1e-3), "unit": UNIT, "steps": n_sus,
+                     "seconds": ms2_max * 1e-3, "ms_per_step": ms2_max / n_sus, "clocks": clk2.summary()}
+        sel.sync()
+
+    # ---- validation of the last step (untimed): histogram, C2 reduce (timed), the law
     hist, totals = sel.histogram(out[0], out[2])
-    reduce_validation(hist, totals, dst=0)     # C2
+    law, e_trials, v_trials, p_shared = (None, None, None, None)
+    if w["rule"] != "argmin":
+        law, e_trials, v_trials, p_shared = law_and_trials(w, sel, alpha)
+    if world > 1:
+        h_s, t_s = hist.clone(), totals.clone()
+        reduce_validation(h_s, t_s, dst=0)    # warm
+        barrier()
+        e0, e1 = ev_pair()
+        e0.record(stream)
+        reduce_validation(hist, totals, dst=0)     # C2
+        e1.record(stream)
+        e1.synchronize()
+        collectives = dict(collectives or {})
+        collectives.update({"c2_reduce_ms": max_over_ranks(e0.elapsed_time(e1), device),
+                            "c2_bytes": 8 * (M + 1) + 16, "backend": dist.get_backend()})
+        if law is not None and w["kind"] == "rows":
+            # per-rank row laws and trial expectations: summed (a shared vector's law is
+            # the same on every rank)
+            extra = torch.stack([torch.as_tensor(e_trials, dtype=torch.float64, device=device),
+                                 torch.as_tensor(v_trials, dtype=torch.float64, device=device)])
+            dist.all_reduce(law)
+            dist.all_reduce(extra)
+            e_trials, v_trials = extra[0], extra[1]
+    if law is not None and w["kind"] == "shared":
+        e_trials, v_trials = e_trials * K_total, v_trials * K_total   # per selection -> all ranks
     trials_sum = int(totals[0].item())
     rejected = int(totals[1].item())
     if w["rule"] == "argmin":
         calls = K * ((M + 3) // 4 + 1)          # M election draws (4 per call) + tau
     else:
         calls = int(((out[2].to(torch.int64) + 1) // 2).sum().item()) + K   # Philox calls of the last launch
+
+    validation = {"seed": seed, "gen_seed": 14040027, "max_trials": w["max_trials"],
+                  "trials_sum_last_step": trials_sum, "rejected_last_step": rejected,
+                  "mean_trials": trials_sum / K_total}
+    if law is not None and rank == 0:
+        h = hist.double().cpu().numpy()
+        lw = law.cpu().numpy()
+        # the law is over the selections that can fire (all-zero rows are rejected by definition)
+        validation["chi2_vs_exact_law"] = chi2_pooled(h[:M], lw * (h[:M].sum() / max(lw.sum(), 1e-300)))
+        n = h[:M].sum()
+        pj = lw / lw.sum()
+        validation["mse"] = float(np.mean((pj - h[:M] / max(n, 1)) ** 2))          # PAPER.md:421-423
+        validation["mse_exact_sampler_expectation"] = float(np.sum(pj * (1 - pj)) / (M * max(n, 1)))
+        if w["rule"] == "classic":
+            e_t, v_t = float(e_trials), float(v_trials)
+            acc = {"p_hat": (K_total - rejected) / trials_sum if trials_sum else None,
+                   "expected_trials_sum": e_t, "z_trials_sum": (trials_sum - e_t) / math.sqrt(v_t) if v_t > 0 else None}
+            if p_shared is not None:
+                acc["p"] = float(p_shared)       # a0 / (M alpha_max), BASELINE.json configs[2]
+            else:
+                acc["p_harmonic"] = K_total / e_t   # K / sum_r 1/p_r over the rows
+            validation["acceptance"] = acc
 
     # SURVEY.md 8(d): useful-trial fraction = sum(trials) / trials computed; a team of g lanes
     # computes whole rounds of 2g canonical trials (g = 32 on the matrix path)
@@ -397,15 +577,15 @@ def run_gpuar(args, w, rank, world, local_rank):
                            "useful_trial_fraction": useful / computed if computed else None}
 
     peaks = measured_peaks()
-    clocks = clk.summary()
     if w["kind"] == "rows":
         bytes_per_launch = K * (4 * M + 12)
-        achieved = bytes_per_launch / (ms_step * 1e-3) / 1e9
+        ms_rank_step = ms / args.steps
+        achieved = bytes_per_launch / (ms_rank_step * 1e-3) / 1e9
         peak = float(peaks["hbm_gbs"])
-        traffic = ncu_traffic(args.config)
+        traffic = ncu_traffic(args.config) if w["rule"] == "classic" else None
         # diagnostic: the same row pipeline streaming the matrix with only the alpha_max /
         # alpha_0 reduction (gpuar_row_stats, no trials) -- what the pipeline itself can read
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0, e1 = ev_pair()
         sel.row_stats()
         n_rs = 20
         e0.record(stream)
@@ -417,7 +597,9 @@ def run_gpuar(args, w, rank, world, local_rank):
         roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                     "traffic": traffic, "peak_source": peaks["_source"] + " hbm_gbs (copy)",
                     "bytes_per_selection": 4 * M + 12, "frac_of_8TBs": achieved / 8000.0,
-                    "row_stats_stream_gbs": rs_gbs}
+                    "row_stats_stream_gbs": rs_gbs, "per": "rank 0's launches (CUDA events on its stream)"}
+        if sustained:
+            sustained["roofline_frac"] = K * (4 * M + 12) / (sus_ms_rank / sustained["steps"] * 1e-3) / 1e9 / peak
     else:
         achieved = calls / (ms_step * 1e-3) / 1e9
         mhz = float(peaks.get("sm_max_mhz", 1965.0))
@@ -445,12 +627,14 @@ def run_gpuar(args, w, rank, world, local_rank):
             sel.select_host(host, K=K, out=hout)
         dt = time.perf_counter() - t0
         dt_max = max_over_ranks(dt, device)
-        e2e = {"value": K * world * args.e2e_steps / dt_max, "unit": UNIT,
+        e2e = {"value": K_total * args.e2e_steps / dt_max, "unit": UNIT,
                "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": 12 * K, "steps": args.e2e_steps,
                # the bound of this number: host<->device bytes per second through PCIe
                "pcie_gbs_per_rank": (h2d + 12 * K) * args.e2e_steps / dt_max / 1e9,
                "timer": "host wall clock around synchronous gpuar_select_host, max over ranks"}
         del host
+        if w["kind"] == "shared":
+            sel.set_propensities(alpha)           # select_host registered its own staged copy
 
     # Short calls: the same selections replayed from a CUDA graph of
     # consecutive gpuar_select launches (an even number: alternate launches use alternate
@@ -470,7 +654,7 @@ def run_gpuar(args, w, rank, world, local_rank):
                     for _ in range(n_calls):
                         sel.select(K, out=out)
                 cg.replay()
-                g0, g1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                g0, g1 = ev_pair()
                 reps = 20
                 g0.record(gs)
                 for _ in range(reps):
@@ -484,12 +668,34 @@ def run_gpuar(args, w, rank, world, local_rank):
         except Exception as exc:                   # informational only
             graph = {"error": str(exc)[:200]}
 
+    # Strong-scaling split beside a weak N > 1 run: K = the config's K in TOTAL over the
+    # ranks (SURVEY.md §8(d) c4 "strong-scaled over G"), contiguous shards of the global
+    # selections; the matrix rows are regenerated for the shard (each rank its own).
+    strong = None
+    if world > 1 and args.scaling == "weak":
+        s0s, Ks = shard(w["K"], rank, world)
+        if w["kind"] == "rows":
+            import synth
+            import synth.gpu as sg
+            sub = alpha[:Ks]
+            sg.fill_rows(sub, torch.from_numpy(synth.yeast_rates(M)).to(device), synth.GEN_SEED, s0s)
+            sel.set_propensities(sub)
+        sel.set_selection_offset(s0s)
+        o2 = tuple(t[:Ks] for t in out)
+        for _ in range(3):
+            sel.select(Ks, out=o2)
+        ms_s, _, _ = timed(args.steps, Ks, o2)
+        ms_s = max_over_ranks(ms_s, device)
+        strong = {"value": w["K"] * args.steps / (ms_s * 1e-3), "unit": UNIT, "K_total": w["K"],
+                  "K_per_gpu_max": max(shard(w["K"], r, world)[1] for r in range(world)),
+                  "ms_per_step": ms_s / args.steps, "steps": args.steps}
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
         threads = os.cpu_count() or 1
         rate, n, dt = oracle_rate(w, args.cpu_seconds, threads,
                                   max_rows=(1 << 17) if w["kind"] == "rows" else None)
-        cpu = {"value": rate, "unit": UNIT, "cores": threads, "kind": "oracle",
+        cpu = {"value": rate, "unit": UNIT, "cores": threads, "kind": "oracle", "cpu_model": cpu_model(),
                "sample": f"first {n} of {K} selections of the same workload, re-run on successive epochs "
                          f"for {dt:.1f} s (OpenMP over selections)"}
         # the same oracle on one host thread (a shorter sample)
@@ -497,14 +703,29 @@ def run_gpuar(args, w, rank, world, local_rank):
                                      max_rows=(1 << 14) if w["kind"] == "rows" else None)
         cpu["value_1thread"] = rate1
         cpu["sample_1thread"] = f"first {n1} selections, {dt1:.1f} s, one thread"
+        # the oracle's inverse-transform linear search on the same
+        # workload, all cores and one thread -- the classic method the paper argues against
+        if w["rule"] == "classic":
+            wi = dict(w, rule="it")
+            r_it, n_it, dt_it = oracle_rate(wi, min(3.0, args.cpu_seconds), threads,
+                                            max_rows=(1 << 17) if w["kind"] == "rows" else None)
+            r_it1, n_it1, dt_it1 = oracle_rate(wi, min(2.0, args.cpu_seconds), 1,
+                                               max_rows=(1 << 14) if w["kind"] == "rows" else None)
+            cpu["it_linear_search"] = {"value": r_it, "cores": threads, "value_1thread": r_it1,
+                                       "sample": f"first {n_it} selections ({dt_it:.1f} s, all cores); "
+                                                 f"first {n_it1} ({dt_it1:.1f} s, one thread)"}
 
     if rank == 0:
         res = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
-            "warmup": max(args.warmup, 3), "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
-            "vs_baseline": None, "dtype": "f32", "data": "synthetic (seeded synth/ generators)",
-            "config": {"workload": w["desc"], "M": M, "K_per_gpu": K, "K_total": K * world,
-                       "dist": w["dist"], "parallelism": f"selections sharded over {world} GPU(s), no data-path collective",
+            "warmup": max(args.warmup, 3), "ms_per_step": ms_step, "higher_is_better": True,
+            "scaling": args.scaling, "vs_baseline": None, "dtype": "f32", "data": "synthetic (seeded synth/ generators)",
+            "config": {"workload": w["desc"] if args.scaling == "weak" else
+                       w["desc"].replace("per GPU", "in total"),
+                       "M": M, "K_per_gpu": K, "K_total": K_total,
+                       "dist": w["dist"], "rule": w["rule"], "max_trials": w["max_trials"],
+                       "parallelism": f"selections sharded over {world} GPU(s) ({args.scaling} scaling), "
+                                      "no data-path collective",
                        "l2": ("inputs larger than L2 (%.2f GB/GPU), no flush" % (K * M * 4 / 1e9)) if w["kind"] == "rows"
                        else "shared vector resident in smem/L2 by design; outputs 12 B/selection",
                        "path": path},
@@ -513,15 +734,19 @@ def run_gpuar(args, w, rank, world, local_rank):
             "e2e": e2e,
             "gpu_launches": args.steps,
             "clocks": clocks,
+            "sustained": sustained,
             "graph_steady_state": graph,
-            "validation": {"trials_sum_last_step": trials_sum, "rejected_last_step": rejected,
-                           "mean_trials": trials_sum / (K * world)},
+            "collectives": collectives,
+            "strong_scaling": strong,
+            "validation": validation,
             "trials": trials_info,
         }
+        if args.oversubscribe:
+            res["oversubscribed"] = {"gpus_visible": torch.cuda.device_count(),
+                                     "note": "ranks share GPUs (dry run): not a scaling measurement"}
         if w["rule"] == "argmin":
             # the paper's Table 1 metric on the last step's histogram and
             # its own K20 timing as context
-            import numpy as np
             h = hist[:M].double().cpu().numpy()
             a = alpha.double().cpu().numpy()
             res["config"]["rule"] = f"argmin (paper's printed election + selection), w={w['w']}"
@@ -561,7 +786,7 @@ def run_ssa(args, w, rank, world, local_rank):
     device = torch.device("cuda", local_rank)
     torch.cuda.set_device(device)
     M, K, inner = w["M"], w["K"], w["inner"]
-    inp = make_inputs(w, rank, device)
+    inp = make_inputs(w, weak_shard(K, rank)[0], K, device)
     sel = Selector(M, K, 20140327, device=local_rank)
     sel.set_selection_offset(weak_shard(K, rank)[0])
     n = inp["net"]
@@ -594,7 +819,11 @@ def run_ssa(args, w, rank, world, local_rank):
     sel.sync()
     ms = max_over_ranks(ev0.elapsed_time(ev1), device)
     events = int(total.sum().item())
-    events_all = int(max_over_ranks(float(events), device)) * world  # weak scaling: equal work per rank
+    # realizations halt or reject at different times on each rank: sum the ranks' events
+    ev_t = torch.tensor([events], dtype=torch.int64, device=device)
+    if world > 1:
+        torch.distributed.all_reduce(ev_t)
+    events_all = int(ev_t.item())
     value = events_all / (ms * 1e-3)
     if rank == 0:
         cpu = None
@@ -615,18 +844,61 @@ def run_ssa(args, w, rank, world, local_rank):
     sel.close()
 
 
+def free_port() -> int:
+    import socket
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        return sk.getsockname()[1]
+
+
+def self_launch(args) -> int:
+    """--gpus N without a launcher: run this script as N ranks under torch.distributed.run
+    (one process per GPU, rendezvous on 127.0.0.1) and return its exit code.  Refuses when
+    fewer than N GPUs are visible, unless --oversubscribe (ranks then share GPUs over gloo)."""
+    import torch
+    n_vis = torch.cuda.device_count()
+    if n_vis < args.gpus and not args.oversubscribe:
+        print(f"bench.py: --gpus {args.gpus} needs {args.gpus} visible GPUs, found {n_vis} "
+              "(--oversubscribe shares GPUs between ranks for a dry run)", file=sys.stderr, flush=True)
+        return 2
+    argv = list(sys.argv[1:])
+    if n_vis < args.gpus and "--dist-backend" not in " ".join(argv):
+        argv += ["--dist-backend", "gloo"]      # NCCL refuses two ranks on one GPU
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr=127.0.0.1", f"--master-port={free_port()}", os.path.abspath(__file__), *argv]
+    env = dict(os.environ)
+    env.setdefault("OMP_NUM_THREADS", "1")
+    return subprocess.call(cmd, env=env)
+
+
 def main():
     args = parse()
     w = workload(args)
+    if args.gpus < 1:
+        raise SystemExit("bench.py: --gpus must be >= 1")
+    launched = "WORLD_SIZE" in os.environ
+    if args.impl == "reference":
+        # the oracle arm runs on rank 0's host cores only; without a launcher there is
+        # nothing to spawn (the other ranks would exit at once)
+        run_reference(args, w, int(os.environ.get("RANK", "0")), int(os.environ.get("WORLD_SIZE", str(args.gpus))))
+        return
+    if not launched and args.gpus > 1:
+        sys.exit(self_launch(args))
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
-    if args.impl == "reference":
-        run_reference(args, w, rank, world)
-        return
+    if world != args.gpus:
+        raise SystemExit(f"bench.py: --gpus {args.gpus} but the launcher started WORLD_SIZE={world} ranks")
     import torch
     import torch.distributed as dist
-    local_rank = local_rank % max(1, torch.cuda.device_count())
+    n_vis = torch.cuda.device_count()
+    if n_vis < 1:
+        raise SystemExit("bench.py: no CUDA device visible (the GPU-AR arm has no CPU fallback)")
+    if local_rank >= n_vis:
+        if not args.oversubscribe:
+            raise SystemExit(f"bench.py: local rank {local_rank} has no GPU of its own ({n_vis} visible); "
+                             "--oversubscribe for a shared-GPU dry run")
+        local_rank %= n_vis
     if world > 1:
         torch.cuda.set_device(local_rank)
         if args.dist_backend == "nccl":

@@ -161,12 +161,17 @@ void plan_shared(gpuar_handle* h) {
     nb[i] = n;
     best_threads = std::max(best_threads, n * blocks[i]);
   }
+  h->sh_grid = 0;
   for (int i = 2; i >= 0; --i) {
     if (nb[i] > 0 && 4 * nb[i] * blocks[i] >= 3 * best_threads) {
       h->sh_block = blocks[i];
       h->sh_grid = nb[i] * h->num_sms;
       break;
     }
+  }
+  if (h->sh_grid <= 0) {  // no size qualified (an unsupported GPUAR_SH_BLOCK, or the
+    h->sh_block = 256;     // occupancy query failed): one 256-thread CTA per SM
+    h->sh_grid = h->num_sms;
   }
 }
 
@@ -237,7 +242,7 @@ int launch_select(gpuar_handle* h, const float* alpha, int64_t rows, int64_t ld,
     } else {
       p.phase = h->ticket_phase;
       {
-        const uint64_t nwarps = (uint64_t)h->sh_grid * (uint64_t)h->sh_block / 32u;
+        const uint64_t nwarps = std::max<uint64_t>(1u, (uint64_t)h->sh_grid * (uint64_t)h->sh_block / 32u);
         const uint64_t fair = std::max<uint64_t>(1u, (uint64_t)K / nwarps);
         uint64_t first = fair / 2u;
         if (fair <= 4u) {

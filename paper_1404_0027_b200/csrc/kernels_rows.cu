@@ -17,7 +17,11 @@
 //    formed once per block of rows at the output flush.
 // Row 4116 bytes is not a multiple of 16, so no 2-D tensor map can describe the matrix;
 // each row's copy covers [floor16(start), ceil16(end)) -- at most 15 extra bytes on
-// each side, always inside 16-byte chunks that hold row data.
+// each side, always inside 16-byte chunks that hold row data -- EXCEPT where ceil16(end)
+// passes the end of the caller's buffer (the last row's last element, for the last 1-3
+// rows of the matrix): those rows' copies stop at floor16(buffer end) and the <= 3 words
+// after it are loaded by lanes 0-2 into the slot, so nothing outside [base, base +
+// ((K-1) ld + M) * 4) is ever read (include/gpuar.h).
 #include <algorithm>
 
 #include "gpuar_internal.cuh"
@@ -200,13 +204,19 @@ __global__ void __launch_bounds__(MAXW * 32, 1) select_rows_kernel(const RowsPar
     w.r += last ? jump : 1u;
     w.pos = last ? 0u : w.pos + 1u;
   };
+  // The caller's buffer ends after the last row's M-th element; rows >= r_tail have a
+  // 16-byte hull that passes that end (at most 3 rows; monotone in r).
+  const uint64_t buf_end = (uint64_t)(K - 1u) * row_bytes + 4ull * M;
+  const uint64_t buf_end16 = buf_end & ~15ull;
+  uint32_t r_tail = K;
+  while (r_tail > 0u && ((((uint64_t)(r_tail - 1u) * row_bytes + 4ull * M + 15ull) & ~15ull) > buf_end)) --r_tail;
   auto issue = [&](uint32_t r, uint32_t slot) {
     const uint64_t off = (uint64_t)r * row_bytes;
     const uint64_t a = off & ~15ull;
-    const uint64_t e = (off + 4ull * M + 15ull) & ~15ull;
+    const uint64_t e = r < r_tail ? (off + 4ull * M + 15ull) & ~15ull : buf_end16;  // >= a
     const uint32_t bytes = (uint32_t)(e - a);
-    mbar_arrive_expect_tx_s(bars_s + 8u * slot, bytes);
-    bulk_g2s_s(ring_s + slot * SB, base + a, bytes, bars_s + 8u * slot, policy);
+    mbar_arrive_expect_tx_s(bars_s + 8u * slot, bytes);  // 0 bytes: a plain arrive
+    if (bytes != 0u) bulk_g2s_s(ring_s + slot * SB, base + a, bytes, bars_s + 8u * slot, policy);
   };
   Walk cur{wg << lb, 0u};
   Walk pre = cur;  // row n + S: the next row to prefetch into the slot row n frees
@@ -255,6 +265,15 @@ __global__ void __launch_bounds__(MAXW * 32, 1) select_rows_kernel(const RowsPar
     // The slot holds the row's 16-byte hull: element j sits at word lead + j.
     const uint32_t lead = (r * row_bytes & 15u) >> 2;
     const uint32_t row_s = ring_s + slot * SB + 4u * lead;
+    if (r >= r_tail) {  // (warp-uniform) the words past floor16(buffer end): plain loads
+      const uint64_t off = (uint64_t)r * row_bytes;
+      const uint64_t t0 = max(off, buf_end16);
+      const uint32_t nt = (uint32_t)((off + 4ull * M - t0) >> 2);  // <= 3
+      if (lane < nt)
+        sts_f32(ring_s + slot * SB + (uint32_t)(t0 - (off & ~15ull)) + 4u * lane,
+                __ldg(reinterpret_cast<const float*>(base + t0) + lane));
+      __syncwarp();
+    }
 
     // ---- alpha_max (max of bit patterns) and alpha_0 in the fixed order of row_reduce
     uint32_t mx;

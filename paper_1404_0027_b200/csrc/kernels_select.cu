@@ -429,7 +429,9 @@ __global__ void __launch_bounds__(1024, 1) select_shared_kernel(const SharedPara
   pool_init(pl, K, nwarps, warp_global, first, grab, P.ctr->next[P.phase], P.no_prefetch == 0u);
   const TrialStream ts(P.seed_lo, P.seed_hi, P.epoch);
   if (g == 1u) {
-    if (st.p <= 0.25f)
+    // two calls per round exactly where choose_team priced them (1/128 <= p <= 1/4); a
+    // forced g = 1 (GPUAR_TEAM) outside that range runs the one-call loop
+    if (st.p <= 0.25f && st.p >= 1.0f / 128.0f)
       lane_loop<PATH, 2>(P, ts, sbase, pl);
     else
       lane_loop<PATH, 1>(P, ts, sbase, pl);

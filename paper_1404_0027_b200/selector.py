@@ -19,6 +19,27 @@ def _ptr(t: torch.Tensor | None):
     return None if t is None else ctypes.c_void_p(t.data_ptr())
 
 
+def _check_buf(t: torch.Tensor | None, n: int, dtype: torch.dtype, device: torch.device | None, name: str,
+               optional: bool = False) -> None:
+    """An output buffer handed to the library as a raw pointer: at least n contiguous
+    elements of `dtype` on `device` (None: host memory) -- the library writes n elements."""
+    if t is None:
+        if optional:
+            return
+        raise ValueError(f"{name} is required")
+    if t.dtype != dtype:
+        raise TypeError(f"{name} must be {dtype}, got {t.dtype}")
+    if device is None:
+        if t.device.type != "cpu":
+            raise ValueError(f"{name} must be a host tensor")
+    elif t.device != device:
+        raise ValueError(f"{name} must be on {device}, got {t.device}")
+    if not t.is_contiguous():
+        raise ValueError(f"{name} must be contiguous")
+    if t.numel() < n:
+        raise ValueError(f"{name} holds {t.numel()} elements, {n} needed")
+
+
 # The current stream's raw cudaStream_t for a device index: torch's own fast accessor when
 # present (a plain int, ~10x cheaper than building a torch.cuda.Stream), else the public API.
 _raw_stream = getattr(torch._C, "_cuda_getCurrentRawStream", None)
@@ -153,6 +174,9 @@ class Selector:
             trials = torch.empty(K, dtype=torch.int32, device=self.device) if with_trials else None
         else:
             idx, tau, trials = out
+            _check_buf(idx, K, torch.int32, self.device, "idx")
+            _check_buf(tau, K, torch.float32, self.device, "tau", optional=True)
+            _check_buf(trials, K, torch.int32, self.device, "trials", optional=True)
         # (no torch device context: the library switches to the handle's device itself;
         # raw integer addresses: ctypes converts them for the void* parameters)
         self._stream()
@@ -168,9 +192,15 @@ class Selector:
         if a.dtype != torch.float32 or a.device.type != "cpu":
             raise TypeError("alpha must be a float32 host array")
         if a.dim() == 1:
+            if a.numel() != self.M or not a.is_contiguous():
+                raise ValueError("shared vector must be contiguous with M elements")
             rows, ld = 1, self.M
-        else:
+        elif a.dim() == 2:
+            if a.shape[1] != self.M or a.stride(1) != 1:
+                raise ValueError("matrix must have M contiguous columns (pitch = stride(0))")
             rows, ld = a.shape[0], a.stride(0)
+        else:
+            raise ValueError("alpha must be 1-D or 2-D")
         K = (rows if rows > 1 else self.K) if K is None else int(K)
         if out is None:
             pin = a.is_pinned()
@@ -179,6 +209,9 @@ class Selector:
             trials = torch.empty(K, dtype=torch.int32, pin_memory=pin)
         else:
             idx, tau, trials = out
+        _check_buf(idx, K, torch.int32, None, "idx")
+        _check_buf(tau, K, torch.float32, None, "tau")
+        _check_buf(trials, K, torch.int32, None, "trials")
         with torch.cuda.device(self.device):
             self._stream()
             check(self._lib.gpuar_select_host(self._h, _ptr(a), rows, ld, K, _ptr(idx), _ptr(tau), _ptr(trials)),
@@ -197,13 +230,20 @@ class Selector:
             check(self._lib.gpuar_set_network(self._h, int(N), int(D), _ptr(reac), _ptr(rate), _ptr(didx), _ptr(dval)),
                   "gpuar_set_network")
         self._net = (reac, rate, didx, dval)
+        self._net_N = int(N)
 
     def ssa_run(self, X: torch.Tensor, t: torch.Tensor, n_steps: int, t_end: float = float("inf"),
                 steps: torch.Tensor | None = None) -> torch.Tensor:
         """gpuar_ssa_run: advance K realizations in place (X (K,N) int32, t (K,) float64)."""
         K = X.shape[0]
+        N = getattr(self, "_net_N", None)
+        if X.dim() != 2 or (N is not None and X.shape[1] != N):
+            raise ValueError("X must be (K, N) with the registered network's N species")
+        _check_buf(X, X.numel(), torch.int32, self.device, "X")
+        _check_buf(t, K, torch.float64, self.device, "t")
         if steps is None:
             steps = torch.zeros(K, dtype=torch.int32, device=self.device)
+        _check_buf(steps, K, torch.int32, self.device, "steps")
         with torch.cuda.device(self.device):
             self._stream()
             check(self._lib.gpuar_ssa_run(self._h, _ptr(X), _ptr(t), _ptr(steps), K, int(n_steps), float(t_end)),
@@ -239,6 +279,10 @@ class Selector:
             hist = torch.zeros(self.M + 1, dtype=torch.int64, device=self.device)
         if totals is None:
             totals = torch.zeros(2, dtype=torch.int64, device=self.device)
+        _check_buf(idx, idx.numel(), torch.int32, self.device, "idx")
+        _check_buf(trials, idx.numel(), torch.int32, self.device, "trials", optional=True)
+        _check_buf(hist, self.M + 1, torch.int64, self.device, "hist")
+        _check_buf(totals, 2, torch.int64, self.device, "totals")
         with torch.cuda.device(self.device):
             self._stream()
             check(self._lib.gpuar_histogram(self._h, _ptr(idx), _ptr(trials), idx.numel(), _ptr(hist), _ptr(totals)),

@@ -1,0 +1,252 @@
+"""GPU parity across every launch geometry and arithmetic branch of the hot path
+(R6: "outputs identical for any G/team/block").
+
+* shared vector: every team size g (GPUAR_TEAM = 1 .. 32, including g = 16 which the model
+  never picks on the test vectors) x CTA size (GPUAR_SH_BLOCK 256 / 1024) x ticket grab
+  (GPUAR_GRAB 1 / the model's) on four acceptance regimes -- p ~ 0.5 (uniform), ~0.15
+  (exponential: the two-call lane loop), ~0.007 (yeast-like) and a Pareto tail (p ~ 3e-3)
+  -- with a ragged K; the two prefilter paths (16-bit brackets, group bounds) at three team
+  sizes; programmatic dependent launch off and ticket prefetch off;
+* the non-FOLD instantiations (alpha_max < 2^-102, where alpha_max * 2^-24 is subnormal):
+  matrix rows (classic and argmin rule), the shared-vector argmin rule and the SSA kernel,
+  with propensities scaled by 2^-110 and 2^-125;
+* the argmin rule's batched leftover Philox calls on the matrix over many rows per warp
+  (rows 8..15 of a 16-row batch, the block jump of the row walk, the refill at
+  n = 16), at three row-block sizes with a selection offset and epoch.
+Every case: idx and trials bit-exact against the oracle, tau within 1e-6 relative."""
+import functools
+
+import numpy as np
+import pytest
+import torch
+
+import oracle
+import synth
+
+pytestmark = pytest.mark.gpu
+
+SEED = synth.SELECT_SEED
+TAU_RTOL = 1e-6
+K_SWEEP = 10_007          # ragged: not a multiple of 32, nor of the stripe count
+
+
+def _check(gpu, ref):
+    idx, tau, trials = (t.cpu().numpy() for t in gpu)
+    mism = np.nonzero(idx != ref["idx"])[0]
+    assert mism.size == 0, f"{mism.size} idx mismatches, first at {mism[:5]}"
+    np.testing.assert_array_equal(trials.view(np.uint32), ref["trials"])
+    tref = ref["tau_ref"]
+    fin = np.isfinite(tref)
+    assert np.array_equal(np.isinf(tau), np.isinf(tref))
+    rel = np.abs(tau[fin].astype(np.float64) - tref[fin]) / tref[fin]
+    assert rel.size == 0 or rel.max() <= TAU_RTOL, rel.max()
+
+
+VECTORS = {
+    "uniform1k": lambda: synth.uniform(1000),
+    "exponential1k": lambda: synth.exponential(1000),
+    "yeast": lambda: synth.yeast_like(),
+    "pareto10k": lambda: synth.pareto(10_000),
+    "exponential70k": lambda: synth.exponential(70_000),     # path 2: 16-bit brackets
+    "pareto300k": lambda: synth.pareto(300_000),             # path 3: group bounds
+}
+
+
+@functools.lru_cache(maxsize=None)
+def _vector_and_ref(name, epoch, s0):
+    a = np.ascontiguousarray(VECTORS[name](), np.float32)
+    return a, oracle.ar_select(a, K_SWEEP, seed=SEED, epoch=epoch, s0=s0, nthreads=8)
+
+
+def _run_shared(monkeypatch, name, env, epoch=2, s0=4321):
+    from paper_1404_0027_b200 import Selector
+    for k, v in env.items():
+        monkeypatch.setenv(k, str(v))
+    a, ref = _vector_and_ref(name, epoch, s0)
+    sel = Selector(a.size, K_SWEEP, SEED)
+    sel.set_selection_offset(s0)
+    sel.epoch = epoch
+    sel.set_propensities(torch.from_numpy(a).cuda())
+    out = sel.select(K_SWEEP)
+    out2 = sel.select(K_SWEEP)             # the next launch uses the other ticket set
+    sel.sync()
+    team = sel.last_team
+    _check(out, ref)
+    ref2 = oracle.ar_select(a, K_SWEEP, seed=SEED, epoch=epoch + 1, s0=s0, nthreads=8)
+    _check(out2, ref2)
+    return sel, team
+
+
+@pytest.mark.parametrize("name", ["uniform1k", "exponential1k", "yeast", "pareto10k"])
+@pytest.mark.parametrize("team", [1, 2, 4, 8, 16, 32])
+@pytest.mark.parametrize("block", [256, 1024])
+@pytest.mark.parametrize("grab", [0, 1])
+def test_shared_geometry_sweep(monkeypatch, name, team, block, grab):
+    env = {"GPUAR_TEAM": team, "GPUAR_SH_BLOCK": block}
+    if grab:
+        env["GPUAR_GRAB"] = grab
+    _, g = _run_shared(monkeypatch, name, env)
+    assert g == team
+
+
+@pytest.mark.parametrize("name", ["exponential70k", "pareto300k"])
+@pytest.mark.parametrize("team", [1, 4, 16, 32])
+def test_prefilter_paths_geometry(monkeypatch, name, team):
+    sel, g = _run_shared(monkeypatch, name, {"GPUAR_TEAM": team})
+    assert g == team and sel.path in ("smem_bracket16", "smem_group_max")
+
+
+@pytest.mark.parametrize("name", ["uniform1k", "yeast", "pareto10k"])
+@pytest.mark.parametrize("env", [{"GPUAR_NO_PDL": 1}, {"GPUAR_NO_PREFETCH": 1}, {"GPUAR_SH_BLOCK": 512},
+                                 {"GPUAR_SH_CTAS_PER_SM": 1, "GPUAR_SH_BLOCK": 256}])
+def test_shared_launch_options(monkeypatch, name, env):
+    _run_shared(monkeypatch, name, env)
+
+
+def test_unsupported_block_falls_back(monkeypatch):
+    # GPUAR_SH_BLOCK outside {256, 512, 1024}: no size qualifies -> one 256-thread CTA per SM
+    # (the host divided by a zero warp count)
+    _run_shared(monkeypatch, "yeast", {"GPUAR_SH_BLOCK": 384})
+
+
+def test_forced_lane_loop_outside_two_call_range(monkeypatch):
+    # g = 1 forced where p < 1/128 (yeast-like, p ~ 0.0068) and p > 1/4 (uniform): the
+    # one-call lane loop runs, not the two-call variant the model never priced there
+    for name in ("yeast", "uniform1k"):
+        _run_shared(monkeypatch, name, {"GPUAR_TEAM": 1})
+
+
+# ---------------------------------------------------------------- non-FOLD branches
+
+@pytest.mark.parametrize("scale_exp", [-110, -125])
+def test_rows_classic_tiny_scale(scale_exp):
+    from paper_1404_0027_b200 import Selector
+    M, K = 1029, 3001
+    host = synth.rows(synth.yeast_rates(M), synth.GEN_SEED, 50, K) * np.float32(2.0 ** scale_exp)
+    assert host.max() < 2.0 ** -102
+    sel = Selector(M, K, SEED)
+    sel.set_selection_offset(50)
+    sel.set_propensities(torch.from_numpy(host).cuda())
+    out = sel.select(K)
+    sel.sync()
+    _check(out, oracle.ar_select(host, K, seed=SEED, s0=50, nthreads=8))
+
+
+@pytest.mark.parametrize("scale_exp", [-110, -125])
+@pytest.mark.parametrize("w", [1.0, 1.5])
+def test_rows_argmin_tiny_scale(scale_exp, w):
+    from paper_1404_0027_b200 import Selector
+    M, K = 1029, 2000
+    host = synth.rows(synth.yeast_rates(M), synth.GEN_SEED, 0, K) * np.float32(2.0 ** scale_exp)
+    sel = Selector(M, K, SEED)
+    sel.set_rule("argmin", w)
+    sel.set_propensities(torch.from_numpy(host).cuda())
+    idx, _, _ = sel.select(K)
+    sel.sync()
+    np.testing.assert_array_equal(idx.cpu().numpy(), oracle.argmin_select(host, K, seed=SEED, w=w, nthreads=8)["idx"])
+
+
+@pytest.mark.parametrize("scale_exp", [-110, -125])
+@pytest.mark.parametrize("M", [64, 1029, 70_000])
+def test_shared_argmin_tiny_scale(scale_exp, M):
+    from paper_1404_0027_b200 import Selector
+    a = (synth.discrete_gaussian(M) if M < 70_000 else synth.exponential(M)) * np.float32(2.0 ** scale_exp)
+    K = 4000 if M < 70_000 else 300
+    sel = Selector(M, K, SEED)
+    sel.set_rule("argmin", 1.0)
+    sel.set_propensities(torch.from_numpy(np.ascontiguousarray(a)).cuda())
+    idx, _, _ = sel.select(K)
+    sel.sync()
+    np.testing.assert_array_equal(idx.cpu().numpy(), oracle.argmin_select(a, K, seed=SEED, w=1.0, nthreads=8)["idx"])
+
+
+def test_ssa_tiny_scale():
+    """The SSA kernel's trials with alpha_max < 2^-102 (ssa_trials<false>): rate constants
+    scaled by 2^-125 (mass-action products stay below 2^-102)."""
+    from paper_1404_0027_b200 import Selector
+    net = synth.yeast_like_network()
+    net = dict(net, rate=(net["rate"] * np.float32(2.0 ** -125)).astype(np.float32))
+    K = 1000
+    X0 = synth.initial_state(net["N"], K)
+    sel = Selector(net["rate"].size, K, SEED)
+    dev = {k: torch.from_numpy(np.ascontiguousarray(net[k])).cuda() for k in ("reac", "rate", "didx", "dval")}
+    sel.set_network(dev["reac"], dev["rate"], dev["didx"], dev["dval"], net["N"])
+    X = torch.from_numpy(np.ascontiguousarray(X0)).cuda()
+    t = torch.zeros(K, dtype=torch.float64, device="cuda")
+    steps = sel.ssa_run(X, t, 20)
+    sel.sync()
+    ref = oracle.ssa_run(net, X0, np.zeros(K), 20, seed=SEED, nthreads=8)
+    np.testing.assert_array_equal(X.cpu().numpy(), ref["X"])
+    np.testing.assert_array_equal(steps.cpu().numpy(), ref["steps"])
+    np.testing.assert_allclose(t.cpu().numpy(), ref["t"], rtol=1e-6)
+
+
+# ---------------------------------------------------------------- batched argmin leftovers
+
+@pytest.mark.parametrize("M", [5, 257, 1029])
+@pytest.mark.parametrize("log2_block", [0, 3, 5])
+def test_argmin_rows_batched_leftovers_many_rows(monkeypatch, M, log2_block):
+    from paper_1404_0027_b200 import Selector
+    monkeypatch.setenv("GPUAR_ROWS_LOG2_BLOCK", str(log2_block))
+    K, s0, epoch = 65_536 + 77, 1_000_003, 9
+    rates = synth.yeast_rates(max(M, 2))[:M].copy()
+    host = synth.rows(rates, synth.GEN_SEED, s0, K)
+    sel = Selector(M, K, SEED)
+    sel.set_rule("argmin", 1.0)
+    sel.set_selection_offset(s0)
+    sel.epoch = epoch
+    sel.set_propensities(torch.from_numpy(host).cuda())
+    idx, tau, _ = sel.select(K)
+    sel.sync()
+    ref = oracle.argmin_select(host, K, seed=SEED, w=1.0, epoch=epoch, s0=s0, nthreads=16)
+    gi = idx.cpu().numpy()
+    mism = np.nonzero(gi != ref["idx"])[0]
+    assert mism.size == 0, f"{mism.size} mismatches, first rows {mism[:8]}"
+    fin = np.isfinite(ref["tau_ref"])
+    rel = np.abs(tau.cpu().numpy()[fin] - ref["tau_ref"][fin]) / ref["tau_ref"][fin]
+    assert rel.max() <= TAU_RTOL
+
+
+# ---------------------------------------------------------------- exact-size allocations, binding checks
+
+def test_matrix_exact_size_allocation():
+    """The matrix path reads nothing past the caller's buffer: matrices whose last element
+    ends mid-16-byte chunk, in exact-size cudaMalloc allocations, under compute-sanitizer
+    memcheck (tests/tail_overread_case.py), and bit-exact against the oracle."""
+    import os
+    import subprocess
+    import sys
+    here = os.path.dirname(os.path.abspath(__file__))
+    script = os.path.join(here, "tail_overread_case.py")
+    plain = subprocess.run([sys.executable, script], capture_output=True, text=True, timeout=600)
+    assert plain.returncode == 0, plain.stdout[-2000:] + plain.stderr[-2000:]
+    san = "/usr/local/cuda/bin/compute-sanitizer"
+    if not os.path.exists(san):
+        pytest.skip("compute-sanitizer not in this image")
+    out = subprocess.run([san, "--tool", "memcheck", "--error-exitcode", "9", sys.executable, script],
+                         capture_output=True, text=True, timeout=900)
+    assert out.returncode == 0, out.stdout[-3000:] + out.stderr[-2000:]
+    assert "ERROR SUMMARY: 0 errors" in out.stdout + out.stderr
+
+
+def test_binding_rejects_bad_output_buffers():
+    from paper_1404_0027_b200 import Selector
+    a = torch.from_numpy(synth.yeast_like()).cuda()
+    sel = Selector(a.numel(), 1000, SEED)
+    sel.set_propensities(a)
+    good = (torch.empty(1000, dtype=torch.int32, device="cuda"), torch.empty(1000, device="cuda"),
+            torch.empty(1000, dtype=torch.int32, device="cuda"))
+    sel.select(1000, out=good)
+    with pytest.raises(ValueError):
+        sel.select(1000, out=(good[0][:999], good[1], good[2]))          # too short
+    with pytest.raises(TypeError):
+        sel.select(1000, out=(good[0].float(), good[1], good[2]))        # wrong dtype
+    with pytest.raises(ValueError):
+        sel.select(1000, out=(good[0].cpu(), good[1], good[2]))          # wrong device
+    with pytest.raises(ValueError):
+        sel.select(500, out=(good[0][::2], good[1], good[2]))            # not contiguous
+    with pytest.raises(ValueError):
+        sel.select_host(np.ones(a.numel() + 1, np.float32), K=10)        # shared vector != M
+    with pytest.raises(ValueError):
+        sel.select_host(np.ones((10, a.numel() + 3), np.float32)[:, :a.numel() + 1], K=10)
+    sel.sync()
