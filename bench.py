@@ -370,14 +370,34 @@ def law_and_trials(w: dict, sel, alpha):
     for every selection; matrix: the row laws summed (chunked, the matrix is 4.3 GB), and
     E[trials] = 1/p_r, Var = (1 - p_r)/p_r^2 with p_r = alpha_0,r / (M alpha_max,r) from
     gpuar_row_stats."""
+    import numpy as np
     import torch
 
     M = w["M"]
     if alpha.dim() == 1:
-        a = alpha.double()
-        law = a / a.sum()
-        amax, a0 = a.max(), a.sum()
-        p = a0 / (M * amax)
+        # The exact law of the discrete draws (DESIGN.md R3/R5): candidate j has
+        # n_j = #{x < 2^32 : (x M) >> 32 = j} of the 2^32 index words and is accepted for
+        # T_j = #{v < 2^24 : fl32(v 2^-24 alpha_max) < alpha_j} of the 2^24 uniforms, so a
+        # trial accepts j with probability n_j T_j / 2^56.  (alpha_j / alpha_0 and
+        # a0 / (M alpha_max) are its continuum limits; on the heavy-tailed c5 vector the
+        # 2^-24 quantisation of u moves p by +0.3 %, 5.7 sigma over 2^21 selections.)
+        a = alpha.detach().cpu().numpy().astype(np.float32)
+        amax = np.float32(a.max())
+        lo = np.zeros(M, np.int64)                 # T_j by bisection: the first v whose
+        hi = np.full(M, 1 << 24, np.int64)         # fl32(v 2^-24 amax) >= alpha_j
+        while np.any(lo < hi):
+            mid = (lo + hi) >> 1
+            u = (mid.astype(np.float32) * np.float32(2.0 ** -24)) * amax
+            ge = u >= a
+            hi = np.where(ge, mid, hi)
+            lo = np.where(ge, lo, mid + 1)
+        T = lo.astype(np.float64)
+        j = np.arange(M + 1, dtype=np.uint64)
+        edge = (j * np.uint64(1 << 32) + np.uint64(M - 1)) // np.uint64(M)   # first x mapping to j
+        n = np.diff(edge).astype(np.float64)
+        wgt = n * T
+        law = torch.as_tensor(wgt / wgt.sum(), device=alpha.device)
+        p = float(wgt.sum() / 2.0 ** 56)
         return law, 1.0 / p, (1.0 - p) / (p * p), p
     amax_r, a0_r = sel.row_stats()
     law = torch.zeros(M, dtype=torch.float64, device=alpha.device)
@@ -559,7 +579,8 @@ def run_gpuar(args, w, rank, world, local_rank):
             acc = {"p_hat": (K_total - rejected) / trials_sum if trials_sum else None,
                    "expected_trials_sum": e_t, "z_trials_sum": (trials_sum - e_t) / math.sqrt(v_t) if v_t > 0 else None}
             if p_shared is not None:
-                acc["p"] = float(p_shared)       # a0 / (M alpha_max), BASELINE.json configs[2]
+                acc["p"] = float(p_shared)       # exact per-trial acceptance of the discrete draws
+                acc["p_continuum"] = float(alpha.double().sum() / (M * alpha.double().max()))  # a0 / (M alpha_max), BASELINE.json configs[2]
             else:
                 acc["p_harmonic"] = K_total / e_t   # K / sum_r 1/p_r over the rows
             validation["acceptance"] = acc
