@@ -92,10 +92,11 @@ def parse():
     ap.add_argument("--K", type=int, default=None, help="selections per GPU")
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--max-trials", type=int, default=None, help="per-selection trial cap (default 2^20)")
-    ap.add_argument("--rule", default=None, choices=["classic", "argmin", "it"])
+    ap.add_argument("--rule", default=None, choices=["classic", "argmin", "it", "it_scan"])
     ap.add_argument("--w", type=float, default=1.0, help="argmin rule threshold multiplier T = w alpha_max")
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-it", action="store_true", help="skip the inverse-transform comparison (matrix configs)")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--dist-backend", default="nccl", help="nccl (default); gloo only to dry-run N ranks on one GPU")
     ap.add_argument("--scaling", default="weak", choices=["weak", "strong"],
@@ -265,7 +266,7 @@ def oracle_pass(w: dict, data, nn: int, epoch: int, threads: int):
     alpha = data[:nn] if w["kind"] == "rows" else data
     if w.get("rule") == "argmin":
         oracle.argmin_select(alpha, nn, seed=20140327, w=w["w"], epoch=epoch, nthreads=threads)
-    elif w.get("rule") == "it":
+    elif w.get("rule") in ("it", "it_scan"):
         oracle.it_select(alpha, nn, seed=20140327, epoch=epoch, nthreads=threads)
     else:
         oracle.ar_select(alpha, nn, seed=20140327, epoch=epoch, max_trials=w["max_trials"], nthreads=threads)
@@ -597,6 +598,25 @@ def run_gpuar(args, w, rank, world, local_rank):
             trials_info = {"team": g, "trials_useful": useful, "trials_computed": computed,
                            "useful_trial_fraction": useful / computed if computed else None}
 
+    # NEXT-3 beside the hot path: the classic inverse
+    # transform on the same rows, as prefix sums + search and as the paper's linear scan,
+    # timed like `value` (the same matrix, events on the launching stream, max over ranks)
+    it_cmp = None
+    if w["kind"] == "rows" and w["rule"] == "classic" and not args.no_it:
+        it_cmp = {}
+        n_it = max(3, min(args.steps, 50))
+        for rule in ("it", "it_scan"):
+            sel.set_rule(rule)
+            for _ in range(3):
+                sel.select(K, out=out)
+            ms_it, _, _ = timed(n_it)
+            ms_it = max_over_ranks(ms_it, device)
+            it_cmp[rule] = {"value": K_total * n_it / (ms_it * 1e-3), "ms_per_step": ms_it / n_it, "steps": n_it,
+                            "hbm_frac": K * (4 * M + 12) / (ms_it / n_it * 1e-3) / 1e9 / float(measured_peaks()["hbm_gbs"])}
+        sel.set_rule("classic")
+        it_cmp["ar_over_it"] = value / it_cmp["it"]["value"]
+        it_cmp["ar_over_it_scan"] = value / it_cmp["it_scan"]["value"]
+
     peaks = measured_peaks()
     if w["kind"] == "rows":
         bytes_per_launch = K * (4 * M + 12)
@@ -757,6 +777,7 @@ def run_gpuar(args, w, rank, world, local_rank):
             "clocks": clocks,
             "sustained": sustained,
             "graph_steady_state": graph,
+            "it_comparison": it_cmp,
             "collectives": collectives,
             "strong_scaling": strong,
             "validation": validation,

@@ -129,16 +129,25 @@ int gpuar_select_host(gpuar_t h, const float *h_alpha, int64_t rows, int64_t ld,
  *     u_j = fl32(v_j T), eligible iff u_j < alpha_j with rating R_j = fl32(u_j / alpha_j),
  *     else R_j = 1; idx = argmin_j R_j (ties to the lowest j), -1 if min R >= 1; trials = M.
  *     Its law is NOT alpha_j / alpha_0 (R1).
- *   GPUAR_RULE_IT (w must be 1; shared vector only): the classic inverse transform, the
- *     direct method the paper replaces: u2 = (x >> 8) 2^-24 from Philox
+ *   GPUAR_RULE_IT (w must be 1): the classic inverse transform, the direct method the paper
+ *     replaces (§Methods "The SSA"): u2 = (x >> 8) 2^-24 from Philox
  *     counter {0, s_g, epoch, 2}; idx = the smallest j with C_j > u2 * alpha_0, C_j the
- *     sequential binary64 prefix sum (computed once per registered vector, O(M)); trials = 1.
- * Applies to later gpuar_select / gpuar_select_host calls (shared vector and matrix; IT:
- * gpuar_select / gpuar_select_host on a matrix return EINVAL).
+ *     SEQUENTIAL binary64 prefix sum fl64(C_{j-1} + alpha_j) and alpha_0 = C_{M-1} (the last
+ *     positive j if rounding ever leaves no crossing); trials = 1 (0 for a degenerate or
+ *     invalid vector/row); tau as for the classic rule with fl32(C_{M-1}).  Shared vector:
+ *     C computed once per registered vector, then one binary search per selection.  Matrix:
+ *     per row, block prefix sums + a search of the crossing block (R24: bit-identical
+ *     to the sequential sums, which a row whose partial sums round recomputes sequentially).
+ *   GPUAR_RULE_IT_SCAN (w must be 1; matrix only): the same selection by a linear scan of the
+ *     row from j = 0 ("iterate in the cumulative distribution"), whose step
+ *     count is random -- the cost the paper holds against IT.  Identical outputs to IT.
+ * Applies to later gpuar_select / gpuar_select_host calls (IT_SCAN with a shared vector:
+ * EINVAL from gpuar_select / gpuar_select_host).
  * Errors: EINVAL (unknown rule, w out of range). */
 #define GPUAR_RULE_CLASSIC 0
 #define GPUAR_RULE_ARGMIN  1
 #define GPUAR_RULE_IT      2
+#define GPUAR_RULE_IT_SCAN 3
 int gpuar_set_rule(gpuar_t h, int rule, float w);
 
 /* NEXT-2: the full SSA loop around the selector.

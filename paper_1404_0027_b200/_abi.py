@@ -12,7 +12,7 @@ import os
 from . import _build
 
 OK, EINVAL, ENOMEM, ECUDA, ENOTSET, EPROPENSITY = 0, -1, -2, -3, -4, -5
-RULE_CLASSIC, RULE_ARGMIN, RULE_IT = 0, 1, 2
+RULE_CLASSIC, RULE_ARGMIN, RULE_IT, RULE_IT_SCAN = 0, 1, 2, 3
 
 _vp = ctypes.c_void_p
 _i64 = ctypes.c_int64

@@ -455,7 +455,7 @@ int gpuar_select(gpuar_t h, int64_t K, int32_t* d_idx, float* d_tau, uint32_t* d
   if (!h || !d_idx || K < 1 || K > h->Kcap) return GPUAR_EINVAL;
   if (h->path == kPathNone) return GPUAR_ENOTSET;
   if (h->rows != 1 && K != h->rows) return GPUAR_EINVAL;
-  if (h->rows != 1 && h->rule == kRuleIT) return GPUAR_EINVAL;  // IT: shared vector only
+  if (h->rows == 1 && h->rule == kRuleITScan) return GPUAR_EINVAL;  // IT linear scan: matrix only
   if (h->offset + (uint64_t)K > (1ull << 32)) return GPUAR_EINVAL;
   DeviceGuard g(h->device);
   if (!g.ok) return GPUAR_ECUDA;
@@ -469,7 +469,7 @@ int gpuar_select_host(gpuar_t h, const float* h_alpha, int64_t rows, int64_t ld,
   if (!h || !h_alpha || !h_idx || !h_tau || !h_trials || K < 1 || K > h->Kcap) return GPUAR_EINVAL;
   if (!(rows == 1 || rows == K)) return GPUAR_EINVAL;
   if (rows != 1 && ld < h->M) return GPUAR_EINVAL;
-  if (rows != 1 && h->rule == kRuleIT) return GPUAR_EINVAL;  // IT: shared vector only
+  if (rows == 1 && h->rule == kRuleITScan) return GPUAR_EINVAL;  // IT linear scan: matrix only
   if (h->offset + (uint64_t)K > (1ull << 32)) return GPUAR_EINVAL;
   DeviceGuard g(h->device);
   if (!g.ok) return GPUAR_ECUDA;
@@ -571,7 +571,7 @@ int gpuar_select_host(gpuar_t h, const float* h_alpha, int64_t rows, int64_t ld,
 
 int gpuar_set_rule(gpuar_t h, int rule, float w) {
   if (!h) return GPUAR_EINVAL;
-  if (rule == GPUAR_RULE_CLASSIC || rule == GPUAR_RULE_IT) {
+  if (rule == GPUAR_RULE_CLASSIC || rule == GPUAR_RULE_IT || rule == GPUAR_RULE_IT_SCAN) {
     if (w != 1.0f) return GPUAR_EINVAL;
   } else if (rule == GPUAR_RULE_ARGMIN) {
     if (!(w >= 1.0f) || !std::isfinite(w)) return GPUAR_EINVAL;

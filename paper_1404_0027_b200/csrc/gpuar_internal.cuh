@@ -45,6 +45,7 @@ enum Rule : int {
   kRuleClassic = 0,  // classic AR, first accept (the north_star hot path)
   kRuleArgmin = 1,   // the paper's printed election + argmin selection
   kRuleIT = 2,       // inverse transform, the classic direct method
+  kRuleITScan = 3,   // the same, per-realization matrix as a linear scan from j = 0
 };
 
 struct SharedParams {
@@ -94,7 +95,7 @@ struct RowsParams {
   uint32_t log2_stages;      // ring depth per warp = 2^log2_stages (1, 2 or 4)
   uint32_t stage_bytes;      // bytes per ring slot (multiple of 16)
   uint32_t stats_only;       // 1: gpuar_row_stats (no trials)
-  int rule;                  // kRuleClassic / kRuleArgmin
+  int rule;                  // kRuleClassic / kRuleArgmin / kRuleIT / kRuleITScan
   float w;                   // argmin rule: T = fl32(w * alpha_max)
   uint32_t log2_block;       // rows per warp block = 2^log2_block (<= 32)
 };

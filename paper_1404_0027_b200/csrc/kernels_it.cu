@@ -18,8 +18,6 @@ namespace gpuar {
 
 namespace {
 
-constexpr uint32_t kTagIT = 2u;
-
 __global__ void it_prefix_kernel(const float* __restrict__ alpha, uint32_t M, double* __restrict__ C) {
   if (threadIdx.x != 0 || blockIdx.x != 0) return;
   double acc = 0.0;

@@ -151,8 +151,119 @@ __device__ __forceinline__ void row_argmin(const Stream& ts, uint32_t sel, uint3
   id = (uint32_t)(best >> 32) < 0x3f800000u ? (int32_t)(uint32_t)best : -1;
 }
 
-// MODE: kRuleClassic / kRuleArgmin (selection), or kModeStats (gpuar_row_stats)
-constexpr int kModeStats = 2;
+// ---------------------------------------------------------------- inverse transform (NEXT-3)
+// The classic direct method on one row (oracle_it_one): idx = the smallest
+// j with C_j > u2 * alpha_0, C_j = fl64(C_{j-1} + alpha_j) the SEQUENTIAL binary64 prefix sum
+// and alpha_0 = C_{M-1} (R24).  A warp reaches the sequential values without the
+// M-long dependent chain when no partial sum rounds: every alpha_j is a multiple of 2^q
+// (q = the ulp exponent of the smallest non-zero alpha_j), so every partial sum in ANY order
+// is a multiple of 2^q, and if alpha_0 < 2^(q+53) each is exact in binary64 -- then
+// C_j = S_j, the exact prefix, which a warp scan computes in any order.  The test uses the
+// warp's own binary64 sum a (a < 2^(q+52) implies the exact sum < 2^(q+53), the sum's
+// relative error being far below 1/2).  Rows failing it (a dynamic range above ~2^(52 -
+// log2 M)) run the oracle's two sequential passes on lane 0.  The yeast-like rows (0.1 ..
+// 953, M = 1029) pass with 2^5 to spare.
+
+// inclusive warp scan in binary64 (exact on rows that pass the test)
+__device__ __forceinline__ double warp_incl_scan(double x, uint32_t lane) {
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const double t = __shfl_up_sync(kFull, x, o);
+    if (lane >= (uint32_t)o) x = __dadd_rn(x, t);
+  }
+  return x;
+}
+
+// Linear scan of elements [j, end) in warp-wide steps of 32 with carry C = C_{j-1}: the first
+// k with C_k > target, or -1.  The number of steps is the row's random crossing position / 32.
+__device__ __forceinline__ int32_t it_scan_from(uint32_t row_s, uint32_t j, uint32_t end, double C, double target,
+                                                uint32_t lane) {
+  for (; j < end; j += 32u) {
+    const uint32_t k = j + lane;
+    const double v = k < end ? (double)lds_f32(row_s + 4u * k) : 0.0;
+    const double Ck = __dadd_rn(C, warp_incl_scan(v, lane));
+    const uint32_t b = __ballot_sync(kFull, k < end && Ck > target);
+    if (b != 0u) return (int32_t)(j + (uint32_t)__ffs(b) - 1u);
+    C = __shfl_sync(kFull, Ck, 31);
+  }
+  return -1;
+}
+
+// The oracle's algorithm verbatim on one lane (rows whose partial sums round): alpha_0 by the
+// sequential sum, then the sequential scan; the last positive j if rounding exhausts it.
+__device__ __noinline__ int32_t it_sequential(uint32_t row_s, uint32_t M, float u2, double& a0) {
+  double C = 0.0;
+  for (uint32_t j = 0; j < M; ++j) C = __dadd_rn(C, (double)lds_f32(row_s + 4u * j));
+  a0 = C;
+  const double target = __dmul_rn((double)u2, a0);
+  C = 0.0;
+  int32_t last = -1;
+  for (uint32_t j = 0; j < M; ++j) {
+    const float a = lds_f32(row_s + 4u * j);
+    C = __dadd_rn(C, (double)a);
+    if (a > 0.0f) last = (int32_t)j;
+    if (C > target) return (int32_t)j;
+  }
+  return last;
+}
+
+// One row by one warp.  SCAN: the paper's "iterate in the cumulative distribution" -- a
+// linear scan from j = 0 (its step count is random).  Otherwise prefix +
+// search: lane l sums the contiguous block [l B, l B + B) (B odd: conflict-free LDS), a warp
+// scan gives the block prefixes, a ballot finds the block holding the crossing and one
+// linear scan of that block (<= ceil(B / 32) steps) the element.  mx: max of the bit patterns
+// (alpha_max, validity).  Outputs id and a0 (= C_{M-1}); nothing when mx flags the row.
+template <bool SCAN>
+__device__ __forceinline__ void row_it(uint32_t row_s, uint32_t M, uint32_t B, uint32_t lane, float u2,
+                                       uint32_t& mx_out, int32_t& id, double& a0) {
+  uint32_t mx = 0, mn = 0xffffffffu;  // mn: min over (bits - 1), i.e. the smallest non-zero - 1
+  double s = 0.0;
+  const uint32_t j0 = lane * B;
+  const uint32_t n = j0 < M ? min(B, M - j0) : 0u;
+  const uint32_t p = row_s + 4u * j0;
+#pragma unroll 4
+  for (uint32_t k = 0; k < n; ++k) {
+    const float v = lds_f32(p + 4u * k);
+    const uint32_t b = __float_as_uint(v);
+    mx = max(mx, b);
+    mn = min(mn, b - 1u);
+    s = __dadd_rn(s, (double)v);
+  }
+  mx = __reduce_max_sync(kFull, mx);
+  mx_out = mx;
+  if (mx >= kInfBits || mx == 0u) return;
+  mn = __reduce_min_sync(kFull, mn) + 1u;  // the smallest non-zero bit pattern
+  const double P = warp_incl_scan(s, lane);
+  a0 = __shfl_sync(kFull, P, 31);
+  // exact iff a0 < 2^(q + 52), q = max(E_min, 1) - 150 the ulp exponent of the smallest value
+  const int q = (int)max(mn >> 23, 1u) - 150;
+  const int ea = (int)(uint32_t)(__double_as_longlong(a0) >> 52) - 1023;  // a0 > 0: floor(log2 a0)
+  id = -1;
+  if (ea <= q + 51) {  // warp-uniform
+    const double target = __dmul_rn((double)u2, a0);
+    if constexpr (SCAN) {
+      id = it_scan_from(row_s, 0u, M, 0.0, target, lane);
+    } else {
+      const uint32_t bl = __ballot_sync(kFull, P > target);  // P_31 = a0 > target always
+      if (bl != 0u) {
+        const uint32_t w = (uint32_t)__ffs(bl) - 1u;
+        const double Ew = __shfl_sync(kFull, __dsub_rn(P, s), w);  // C before block w (exact)
+        id = it_scan_from(row_s, w * B, min(w * B + B, M), Ew, target, lane);
+      }
+    }
+  }
+  if (id < 0) {  // rounding partial sums (or no crossing found): the oracle's passes
+    double a = 0.0;
+    int32_t i = -1;
+    if (lane == 0) i = it_sequential(row_s, M, u2, a);
+    id = __shfl_sync(kFull, i, 0);
+    a0 = __shfl_sync(kFull, a, 0);
+  }
+}
+
+// MODE: kRuleClassic / kRuleArgmin / kRuleIT / kRuleITScan (selection), or kModeStats
+// (gpuar_row_stats)
+constexpr int kModeStats = 8;
 
 template <int MAXW, int MODE>
 __global__ void __launch_bounds__(MAXW * 32, 1) select_rows_kernel(const RowsParams P) {
@@ -237,6 +348,9 @@ __global__ void __launch_bounds__(MAXW * 32, 1) select_rows_kernel(const RowsPar
   left.src = 0;
   left.x = Philox4{0u, 0u, 0u, 0u};
   float nlog = 0.f;  // -ln(u1) of row_of(n0 + lane)
+  constexpr bool kIT = MODE == kRuleIT || MODE == kRuleITScan;
+  float u2v = 0.f;   // inverse transform: u2 of row_of(n0 + lane) (Philox tag 2)
+  const uint32_t itB = ((M + 31u) >> 5) | 1u;  // IT prefix blocks: odd, >= M / 32
   // this lane's buffered outputs for row (block base + lane); tau is formed at the flush,
   // one division per block: tau = -ln(u1) / fl32(alpha_0), with fl32(alpha_0) = 0 for an
   // all-zero row (tau = +inf) and NaN for an invalid one (tau = NaN)
@@ -252,6 +366,9 @@ __global__ void __launch_bounds__(MAXW * 32, 1) select_rows_kernel(const RowsPar
     if ((n & 31u) == 0u && MODE != kModeStats) {
       const uint32_t nn = n + lane;
       nlog = nn < n_rows ? neg_log_u1(P.seed_lo, P.seed_hi, P.s0 + row_of(nn), P.epoch) : 0.f;
+      if constexpr (kIT)
+        u2v = nn < n_rows ? unit24(philox4x32_10(0u, P.s0 + row_of(nn), P.epoch, kTagIT, P.seed_lo, P.seed_hi).x)
+                          : 0.f;
     }
     if constexpr (MODE == kRuleArgmin) {
       if (left.batched && (n & (kLeftRows - 1u)) == 0u) {  // leftovers of rows n .. n+15
@@ -275,12 +392,33 @@ __global__ void __launch_bounds__(MAXW * 32, 1) select_rows_kernel(const RowsPar
       __syncwarp();
     }
 
+    const uint32_t nl32 = cur.pos;  // this row's slot in the block's output buffer
+    if constexpr (kIT) {
+      // ---- inverse transform: alpha_0 = C_{M-1} and the crossing in one routine
+      const float u2 = __shfl_sync(kFull, u2v, n & 31u);
+      uint32_t mx;
+      int32_t id = -1;
+      double a0 = 0.0;
+      row_it<MODE == kRuleITScan>(row_s, M, itB, lane, u2, mx, id, a0);
+      float a0f = 0.f;
+      if (mx >= kInfBits) {  // invalid row: sticky EPROPENSITY
+        a0f = __uint_as_float(0x7fc00000u);
+        id = -1;
+        if (lane == 0) atomicOr(&P.ctr->err, 1u);
+      } else if (mx != 0u) {
+        a0f = __double2float_rn(a0);
+      }
+      if (lane == nl32) {
+        o_id = id;
+        o_a0f = a0f;
+        o_tr = mx != 0u && mx < kInfBits ? 1u : 0u;  // one uniform per selection
+      }
+    } else {
     // ---- alpha_max (max of bit patterns) and alpha_0 in the fixed order of row_reduce
     uint32_t mx;
     double acc;
     row_reduce(row_s, M, lane, mx, acc);
 
-    const uint32_t nl32 = cur.pos;  // this row's slot in the block's output buffer
     if constexpr (MODE == kModeStats) {
       if (lane == nl32) {
         o_a0f = mx < kInfBits ? __uint_as_float(mx) : __uint_as_float(0x7fc00000u);
@@ -323,6 +461,7 @@ __global__ void __launch_bounds__(MAXW * 32, 1) select_rows_kernel(const RowsPar
         o_tr = tr;
       }
     }
+    }
     if (nl32 == bm || n + 1u == n_rows) {  // flush the block: one coalesced store per output
       const uint32_t rl = r - nl32 + lane;
       if constexpr (MODE == kModeStats) {
@@ -355,6 +494,8 @@ template <int MAXW>
 cudaError_t launch_w(const RowsParams& p, int grid, int warps, size_t sh, cudaStream_t st, bool pdl) {
   if (p.stats_only) return launch_pdl(select_rows_kernel<MAXW, kModeStats>, grid, warps * 32, sh, st, pdl, p);
   if (p.rule == kRuleArgmin) return launch_pdl(select_rows_kernel<MAXW, kRuleArgmin>, grid, warps * 32, sh, st, pdl, p);
+  if (p.rule == kRuleIT) return launch_pdl(select_rows_kernel<MAXW, kRuleIT>, grid, warps * 32, sh, st, pdl, p);
+  if (p.rule == kRuleITScan) return launch_pdl(select_rows_kernel<MAXW, kRuleITScan>, grid, warps * 32, sh, st, pdl, p);
   return launch_pdl(select_rows_kernel<MAXW, kRuleClassic>, grid, warps * 32, sh, st, pdl, p);
 }
 
@@ -363,6 +504,8 @@ void set_limits_w(int bytes) {
   set_max_dynamic_smem(select_rows_kernel<MAXW, kRuleClassic>, bytes);
   set_max_dynamic_smem(select_rows_kernel<MAXW, kRuleArgmin>, bytes);
   set_max_dynamic_smem(select_rows_kernel<MAXW, kModeStats>, bytes);
+  set_max_dynamic_smem(select_rows_kernel<MAXW, kRuleIT>, bytes);
+  set_max_dynamic_smem(select_rows_kernel<MAXW, kRuleITScan>, bytes);
 }
 
 }  // namespace

@@ -16,6 +16,7 @@ constexpr uint32_t kPhiloxW1 = 0xBB67AE85u;
 // Stream tags (counter word 3), R12.
 constexpr uint32_t kTagTrials = 0u;
 constexpr uint32_t kTagTau = 1u;
+constexpr uint32_t kTagIT = 2u;       // inverse transform: u2 = word x0 of call 0
 constexpr uint32_t kTagElection = 3u;  // the paper's argmin rule: call j >> 2, word j & 3
 
 struct Philox4 {

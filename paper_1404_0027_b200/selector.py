@@ -119,9 +119,11 @@ class Selector:
 
     def set_rule(self, rule: str = "classic", w: float = 1.0) -> None:
         """gpuar_set_rule: "classic" (first accept, the hot path), "argmin" (the paper's
-        printed election + argmin selection with threshold T = w * alpha_max) or "it" (the
-        classic inverse transform, shared vector only)."""
-        code = {"classic": _abi.RULE_CLASSIC, "argmin": _abi.RULE_ARGMIN, "it": _abi.RULE_IT}[rule]
+        printed election + argmin selection with threshold T = w * alpha_max), "it" (the
+        classic inverse transform: prefix sums + search) or "it_scan" (the same selection by
+        a linear scan of each row, matrix only)."""
+        code = {"classic": _abi.RULE_CLASSIC, "argmin": _abi.RULE_ARGMIN, "it": _abi.RULE_IT,
+                "it_scan": _abi.RULE_IT_SCAN}[rule]
         check(self._lib.gpuar_set_rule(self._h, code, float(w)), "gpuar_set_rule")
 
     def set_max_trials(self, n: int) -> None:

@@ -567,7 +567,7 @@ def test_it_shared_bit_exact(kind, M):
     assert (trials.cpu() == 1).all()
 
 
-def test_it_law_and_rows_refused():
+def test_it_law_and_scan_refused_on_shared_vector():
     from paper_1404_0027_b200 import GpuarError
     a = synth.hand([1, 2, 3, 4])
     sel = _sel(4, 100_000)
@@ -577,12 +577,12 @@ def test_it_law_and_rows_refused():
     h = np.bincount(idx.cpu().numpy(), minlength=4)
     assert oracle.chi2_pvalue(h, oracle.exact_law(a))[1] > 0.001
     sel2 = _sel(4, 8)
-    sel2.set_rule("it")
-    sel2.set_propensities(torch.ones((8, 4), device="cuda"))
+    sel2.set_rule("it_scan")        # the linear scan is a per-row (matrix) method
+    sel2.set_propensities(torch.from_numpy(a).cuda())
     with pytest.raises(GpuarError):
         sel2.select(8)
     with pytest.raises(GpuarError):
-        sel2.select_host(torch.ones((8, 4)))
+        sel2.select_host(torch.from_numpy(a))
 
 
 # ---------------------------------------------------------------- full-size shared-vector configs
