@@ -549,10 +549,21 @@ def test_set_rule_validation():
 
 # ---------------------------------------------------------------- inverse transform (NEXT-3)
 
-@pytest.mark.parametrize("kind,M", [("hand", 4), ("yeast", 1029), ("exponential", 10_000), ("pareto", 100_000)])
+def _wide_vector(M, gen_seed=5):
+    """2^-40 .. 2^40 with zeros: binary64 partial sums round (the prefix kernel's sequential path)."""
+    rng = np.random.default_rng(gen_seed)
+    a = (2.0 ** rng.uniform(-40, 40, M)).astype(np.float32)
+    a[rng.random(M) < 0.3] = 0.0
+    return a
+
+
+@pytest.mark.parametrize("kind,M", [("hand", 4), ("yeast", 1029), ("exponential", 10_000), ("pareto", 100_000),
+                                    ("uniform", 100_000), ("wide", 5_000), ("wide", 1023), ("pareto", 1_000_000)])
 def test_it_shared_bit_exact(kind, M):
-    a = synth.hand([1, 2, 3, 4]) if kind == "hand" else synth.distribution(kind, M)
-    K = 50_000
+    """The prefix C (parallel when no partial sum rounds, else sequential, R24) is
+    bit-identical to the oracle's sequential sums: the selected indices agree exactly."""
+    a = synth.hand([1, 2, 3, 4]) if kind == "hand" else _wide_vector(M) if kind == "wide" else synth.distribution(kind, M)
+    K = 50_000 if M <= 100_000 else 3_000
     sel = _sel(a.size, K)
     sel.set_rule("it")
     sel.set_selection_offset(11)

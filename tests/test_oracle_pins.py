@@ -115,10 +115,13 @@ def test_stats_and_validity():
     assert oracle.stats(a)[1] == 500500.0
 
 
-def test_tau_closed_forms():
-    # SPEC.md:398-400 sampleTau examples: a0=2,u1=e^-2 -> 1; a0=4,u1=1/2 -> ln2/4.  The
-    # oracle's tau is -logf(u1)/fl32(a0) with u1 from stream tag 1; check the closed form
-    # on the tau_ref (binary64) channel: a0 * tau_ref = -ln(u1) in (0, 16.64].
+def test_tau_range_and_exact_scaling():
+    # SPEC.md:398-400's sampleTau examples (a0=2, u1=e^-2 -> 1; a0=4, u1=1/2 -> ln2/4) cannot
+    # be reproduced through the stream: u1 = (2 (x >> 9) + 1) 2^-24 is an odd multiple of
+    # 2^-24 (R10), never e^-2 or 1/2.  What the closed form fixes and this test
+    # checks: a0 * tau_ref = -ln(u1) lies in [-ln(1 - 2^-24), -ln(2^-24)] = (0, 16.64], and
+    # tau scales exactly as 1/a0.  tau's law (a0 tau ~ Exp(1)) is pinned by the KS test in
+    # test_oracle_stats.py and its values by the golden file (tests/golden/ar_seed14040027.txt).
     r = oracle.ar_select([1, 1], 4096, seed=7)
     x = r["tau_ref"] * 2.0
     assert np.all(x > 0) and np.all(x <= -math.log(2.0**-24) + 1e-12)
