@@ -61,6 +61,48 @@ def main():
         io, _, _ = so.select(300)
         so.sync()
         check(io.cpu().numpy(), oracle.argmin_select(ho, 300, seed=SEED, nthreads=8)["idx"], f"rows argmin M={Mo}")
+    # inverse transform on the rows: yeast rows (parallel exact path) mixed with wide-range rows
+    # (sequential fallback), both forms
+    hw = host.copy()
+    rng = np.random.default_rng(3)
+    hw[1::4] = (2.0 ** rng.uniform(-40, 40, hw[1::4].shape)).astype(np.float32)
+    for rule in ("it", "it_scan"):
+        sel = Selector(M, K, SEED)
+        sel.set_rule(rule)
+        sel.set_propensities(torch.from_numpy(hw).cuda())
+        idx, _, _ = sel.select(K)
+        sel.sync()
+        check(idx.cpu().numpy(), oracle.it_select(hw, K, seed=SEED, nthreads=8), f"rows {rule}")
+    # shared IT prefix: parallel (Pareto) and sequential (wide range) paths
+    for a in (synth.pareto(5000), (2.0 ** rng.uniform(-40, 40, 3000)).astype(np.float32)):
+        sel = Selector(a.size, 500, SEED)
+        sel.set_rule("it")
+        sel.set_propensities(torch.from_numpy(a).cuda())
+        idx, _, _ = sel.select(500)
+        sel.sync()
+        check(idx.cpu().numpy(), oracle.it_select(a, 500, seed=SEED, nthreads=8), "shared it prefix")
+    # every shared-vector loop (lane loop with one and two calls, sub-warp teams, warp loop),
+    # three back-to-back launches each (PDL overlap, alternating ticket sets), then a forced
+    # team size and the non-PDL launch
+    for a in (synth.uniform(1000), synth.exponential(10_000), synth.pareto(1000), synth.yeast_like()):
+        K = 20_000
+        sel = Selector(a.size, K, SEED)
+        sel.set_propensities(torch.from_numpy(a).cuda())
+        outs = [sel.select(K) for _ in range(3)]
+        sel.sync()
+        for e, o in enumerate(outs):
+            check(o[0].cpu().numpy(), oracle.ar_select(a, K, seed=SEED, epoch=e, nthreads=8)["idx"], f"shared team {sel.last_team}")
+    for env in ({"GPUAR_TEAM": "16"}, {"GPUAR_TEAM": "8", "GPUAR_NO_PDL": "1", "GPUAR_SH_BLOCK": "256"}):
+        os.environ.update(env)
+        a = synth.pareto(1000)
+        sel = Selector(a.size, 5000, SEED)
+        sel.set_propensities(torch.from_numpy(a).cuda())
+        outs = [sel.select(5000) for _ in range(2)]
+        sel.sync()
+        for e, o in enumerate(outs):
+            check(o[0].cpu().numpy(), oracle.ar_select(a, 5000, seed=SEED, epoch=e, nthreads=8)["idx"], f"forced {env}")
+        for k in env:
+            del os.environ[k]
     # host pipeline
     sel = Selector(M, K, SEED)
     hi, _, _ = sel.select_host(torch.from_numpy(host).pin_memory())

@@ -44,6 +44,8 @@ def run(M, K, ld, mode, seed=11):
     assert lib.gpuar_create(ctypes.byref(h), M, K, seed) == 0
     if mode == "argmin":
         assert lib.gpuar_set_rule(h, _abi.RULE_ARGMIN, 1.0) == 0
+    elif mode in ("it", "it_scan"):
+        assert lib.gpuar_set_rule(h, _abi.RULE_IT if mode == "it" else _abi.RULE_IT_SCAN, 1.0) == 0
     assert lib.gpuar_set_propensities(h, d_a, K, ld) == 0
     if mode == "stats":
         amax_d, a0_d = dmalloc(4 * K), dmalloc(8 * K)
@@ -66,6 +68,8 @@ def run(M, K, ld, mode, seed=11):
         if mode == "argmin":
             ref = oracle.argmin_select(np.ascontiguousarray(rows), K, seed=seed, w=1.0, nthreads=4)
             ok = np.array_equal(idx, ref["idx"])
+        elif mode in ("it", "it_scan"):
+            ok = np.array_equal(idx, oracle.it_select(np.ascontiguousarray(rows), K, seed=seed, nthreads=4))
         else:
             ref = oracle.ar_select(np.ascontiguousarray(rows), K, seed=seed, nthreads=4)
             ok = np.array_equal(idx, ref["idx"]) and np.array_equal(tr, ref["trials"])
@@ -75,6 +79,9 @@ def run(M, K, ld, mode, seed=11):
     return ok
 
 
+MODES = ("classic", "argmin", "stats", "it", "it_scan")
+
+
 def main():
     bad = []
     # (M, K, ld): last-element ends at 4, 8 or 12 bytes into a 16-byte chunk; tiny rows whose
@@ -82,13 +89,13 @@ def main():
     cases = [(2, 333, 2), (1, 7, 1), (1, 6, 1), (3, 5, 3), (1029, 257, 1029), (5, 4097, 7), (7, 100, 7),
              (1029, 3, 1030)]
     for M, K, ld in cases:
-        for mode in ("classic", "argmin", "stats"):
+        for mode in MODES:
             if not run(M, K, ld, mode):
                 bad.append((M, K, ld, mode))
     if bad:
         print("MISMATCH", bad)
         sys.exit(1)
-    print("ok", len(cases) * 3, "cases")
+    print("ok", len(cases) * len(MODES), "cases")
 
 
 if __name__ == "__main__":
