@@ -104,9 +104,10 @@ def main():
         for k in env:
             del os.environ[k]
     # host pipeline
-    sel = Selector(M, K, SEED)
+    Kh = host.shape[0]
+    sel = Selector(M, Kh, SEED)
     hi, _, _ = sel.select_host(torch.from_numpy(host).pin_memory())
-    check(hi.numpy(), oracle.ar_select(host, K, seed=SEED, nthreads=8)["idx"], "select_host")
+    check(hi.numpy(), oracle.ar_select(host, Kh, seed=SEED, nthreads=8)["idx"], "select_host")
     # SSA
     net = synth.yeast_like_network()
     X0 = synth.initial_state(641, 100)
