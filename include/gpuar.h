@@ -109,6 +109,18 @@ int gpuar_set_propensities(gpuar_t h, const float *d_alpha, int64_t rows, int64_
  * d_idx), ENOTSET, ECUDA. */
 int gpuar_select(gpuar_t h, int64_t K, int32_t *d_idx, float *d_tau, uint32_t *d_trials);
 
+/* n_epochs consecutive selects in one call: outputs [n_epochs][K] (epoch e at d_idx + e*K,
+ * and likewise d_tau / d_trials, which may be NULL), bit-identical to n_epochs gpuar_select
+ * calls on the same registration (selection s_g = offset + s at epochs epoch .. epoch +
+ * n_epochs - 1); then epoch += n_epochs.  For a shared vector under the classic rule the
+ * n_epochs * K selections are ONE launch (one work-stealing pool over all of them), so the
+ * per-launch ramp, staging and drain are paid once -- how an SSA driver that keeps the
+ * vector for several steps calls select (§Methods: the selection repeats
+ * every time step); other rules and the matrix run one launch per epoch.
+ * Errors: as gpuar_select, and EINVAL for n_epochs < 1, n_epochs > 65536 or
+ * K * n_epochs >= 2^32. */
+int gpuar_select_epochs(gpuar_t h, int64_t K, int64_t n_epochs, int32_t *d_idx, float *d_tau, uint32_t *d_trials);
+
 /* End-to-end variant for HOST buffers: copies h_alpha (rows x ld floats, or M floats
  * when rows == 1) to the device, selects, and copies the K outputs back, pipelining
  * host->device copies, selection and device->host copies in row chunks on the handle's

@@ -28,6 +28,7 @@ SIGNATURES = {
     "gpuar_set_stream": (_int, [_vp, _vp]),
     "gpuar_set_propensities": (_int, [_vp, _vp, _i64, _i64]),
     "gpuar_select": (_int, [_vp, _i64, _vp, _vp, _vp]),
+    "gpuar_select_epochs": (_int, [_vp, _i64, _i64, _vp, _vp, _vp]),
     "gpuar_select_host": (_int, [_vp, _vp, _i64, _i64, _i64, _vp, _vp, _vp]),
     "gpuar_set_rule": (_int, [_vp, _int, ctypes.c_float]),
     "gpuar_set_network": (_int, [_vp, _i64, _i64, _vp, _vp, _vp, _vp]),

@@ -201,8 +201,10 @@ int plan_rows(gpuar_handle* h) {
   return GPUAR_OK;
 }
 
+// n_epochs > 1 (gpuar_select_epochs; shared vector, classic rule only): one launch works the
+// n_epochs * K items of n consecutive calls, outputs [n_epochs][K].
 int launch_select(gpuar_handle* h, const float* alpha, int64_t rows, int64_t ld, int64_t K, uint64_t s0,
-                  int32_t* idx, float* tau, uint32_t* trials, cudaStream_t st) {
+                  int32_t* idx, float* tau, uint32_t* trials, cudaStream_t st, uint32_t n_epochs = 1) {
   cudaError_t e;
   if (rows == 1) {
     SharedParams p{};
@@ -215,7 +217,10 @@ int launch_select(gpuar_handle* h, const float* alpha, int64_t rows, int64_t ld,
     p.tau = tau;
     p.trials = trials;
     p.M = (uint32_t)h->M;
-    p.K = (uint32_t)K;
+    p.K = (uint32_t)(K * n_epochs);  // work items
+    p.Ksel = (uint32_t)K;
+    p.n_epochs = n_epochs;
+    p.kinv = 1.0f / (float)K;
     p.s0 = (uint32_t)s0;
     p.epoch = h->epoch;
     p.seed_lo = (uint32_t)h->seed;
@@ -243,10 +248,11 @@ int launch_select(gpuar_handle* h, const float* alpha, int64_t rows, int64_t ld,
       p.phase = h->ticket_phase;
       {
         const uint64_t nwarps = std::max<uint64_t>(1u, (uint64_t)h->sh_grid * (uint64_t)h->sh_block / 32u);
-        const uint64_t fair = std::max<uint64_t>(1u, (uint64_t)K / nwarps);
+        const uint64_t Q = (uint64_t)K * n_epochs;
+        const uint64_t fair = std::max<uint64_t>(1u, Q / nwarps);
         uint64_t first = fair / 2u;
         if (fair <= 4u) {
-          const uint64_t stripe = ((uint64_t)K + kStripes - 1u) / kStripes;
+          const uint64_t stripe = (Q + kStripes - 1u) / kStripes;
           const uint64_t per = std::max<uint64_t>(1u, nwarps / kStripes);  // fewest warps any stripe has
           first = (stripe + per - 1u) / per;
         }
@@ -462,6 +468,31 @@ int gpuar_select(gpuar_t h, int64_t K, int32_t* d_idx, float* d_tau, uint32_t* d
   const int st = launch_select(h, h->alpha, h->rows, h->ld, K, h->offset, d_idx, d_tau, d_trials, h->stream);
   if (st == GPUAR_OK) ++h->epoch;
   return st;
+}
+
+int gpuar_select_epochs(gpuar_t h, int64_t K, int64_t n_epochs, int32_t* d_idx, float* d_tau, uint32_t* d_trials) {
+  if (!h || !d_idx || K < 1 || K > h->Kcap || n_epochs < 1 || n_epochs > 65536) return GPUAR_EINVAL;
+  if ((uint64_t)K * (uint64_t)n_epochs > 0xffffffffull) return GPUAR_EINVAL;
+  if (h->path == kPathNone) return GPUAR_ENOTSET;
+  if (h->rows != 1 && K != h->rows) return GPUAR_EINVAL;
+  if (h->rows == 1 && h->rule == kRuleITScan) return GPUAR_EINVAL;
+  if (h->offset + (uint64_t)K > (1ull << 32)) return GPUAR_EINVAL;
+  DeviceGuard g(h->device);
+  if (!g.ok) return GPUAR_ECUDA;
+  if (h->rows == 1 && h->rule == kRuleClassic && n_epochs > 1) {
+    // one launch for all epochs: the fixed cost of a launch (ramp, staging, drain) is paid once
+    const int st = launch_select(h, h->alpha, 1, h->ld, K, h->offset, d_idx, d_tau, d_trials, h->stream,
+                                 (uint32_t)n_epochs);
+    if (st == GPUAR_OK) h->epoch += (uint32_t)n_epochs;
+    return st;
+  }
+  for (int64_t e = 0; e < n_epochs; ++e) {  // other rules and the matrix: one launch per epoch
+    const int st = launch_select(h, h->alpha, h->rows, h->ld, K, h->offset, d_idx + e * K,
+                                 d_tau ? d_tau + e * K : nullptr, d_trials ? d_trials + e * K : nullptr, h->stream);
+    if (st != GPUAR_OK) return st;
+    ++h->epoch;
+  }
+  return GPUAR_OK;
 }
 
 int gpuar_select_host(gpuar_t h, const float* h_alpha, int64_t rows, int64_t ld, int64_t K, int32_t* h_idx,

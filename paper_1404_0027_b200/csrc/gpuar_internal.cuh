@@ -75,7 +75,28 @@ struct SharedParams {
                              // (static chunks that cover each stripe: no tickets at all)
   uint32_t no_prefetch;      // tuning: 1 = fetch tickets on demand
   uint32_t phase;            // ticket set of this launch (DevCounters::next)
+  // multi-epoch launches (gpuar_select_epochs): K above is the number of work items
+  // n_epochs * Ksel; item q is selection q mod Ksel at epoch + q / Ksel, output slot q
+  uint32_t Ksel;             // selections per epoch
+  uint32_t n_epochs;         // epochs in this launch (1: a plain gpuar_select)
+  float kinv;                // fl32(1 / Ksel): q / Ksel to within one, then corrected
 };
+
+// Item q of a multi-epoch launch -> (epoch offset e, selection s): q = e * Ksel + s.  The
+// binary32 estimate is within one of q / Ksel for e < 2^16 (relative error < 2^-22); one
+// exact correction step in 64-bit arithmetic.
+__device__ __forceinline__ void split_item(uint32_t q, uint32_t Ksel, float kinv, uint32_t& e, uint32_t& s) {
+  e = __float2uint_rz(__fmul_rn(__uint2float_rn(q), kinv));
+  long long r = (long long)q - (long long)e * Ksel;
+  if (r < 0) {
+    --e;
+    r += Ksel;
+  } else if (r >= (long long)Ksel) {
+    ++e;
+    r -= Ksel;
+  }
+  s = (uint32_t)r;
+}
 
 struct RowsParams {
   const float* alpha;        // K rows, pitch ld floats, 16-byte aligned base

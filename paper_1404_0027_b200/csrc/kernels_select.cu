@@ -47,6 +47,29 @@ __device__ __forceinline__ bool accept(uint32_t x, uint32_t j, uint32_t sbase, c
   }
 }
 
+// Round-1 words of work item q: selection s0 + q at the launch's epoch, or (multi-epoch
+// launch) selection s0 + q mod Ksel at epoch + q / Ksel.  elo is lo(M1 * epoch).
+template <bool MULTI>
+__device__ __forceinline__ void item_words(const SharedParams& P, const TrialStream& ts, uint32_t q, uint32_t& sel,
+                                           uint32_t& elo) {
+  if constexpr (MULTI) {
+    uint32_t e, s;
+    split_item(q, P.Ksel, P.kinv, e, s);
+    ts.words(P.epoch + e, P.s0 + s, sel, elo);
+  } else {
+    sel = ts.sel_word(P.s0 + q);
+    elo = ts.e_lo;
+  }
+}
+
+template <bool MULTI>
+__device__ __forceinline__ Philox4 item_call(const TrialStream& ts, uint32_t c, uint32_t sel, uint32_t elo) {
+  if constexpr (MULTI)
+    return ts.call(c, sel, elo);
+  else
+    return ts(c, sel);  // e_lo from the (uniform) stream
+}
+
 // Work distribution: the K selections are cut into kStripes contiguous stripes; warp w
 // belongs to stripe w % kStripes, takes a static first chunk of it, then grabs `grab`
 // selections at a time from the stripe's ticket until the stripe is exhausted.  kStripes
@@ -137,7 +160,7 @@ __device__ __forceinline__ uint32_t pool_take(Pool& pl, uint32_t need, uint32_t 
 // Trial phase of one warp with sub-warp teams (1 < g < 32 lanes per selection).
 // Fast path: one Philox call + two gathers + one vote per round; team bookkeeping only
 // when some team of the warp finished a selection.
-template <int PATH>
+template <int PATH, bool MULTI>
 __device__ __forceinline__ void trial_loop(const SharedParams& P, const TrialStream& ts, uint32_t sbase, uint32_t g,
                                            Pool pl) {
   const uint32_t M = P.M;
@@ -151,6 +174,7 @@ __device__ __forceinline__ void trial_loop(const SharedParams& P, const TrialStr
 
   uint32_t my = kNone;  // local selection of this lane's team
   uint32_t sel = 0;     // its round-1 Philox word
+  uint32_t elo = 0;     // (multi-epoch) its epoch word
   uint32_t c = 0;       // this lane's Philox call within the selection
 
   while (true) {
@@ -159,7 +183,7 @@ __device__ __forceinline__ void trial_loop(const SharedParams& P, const TrialStr
       const uint32_t got = pool_take(pl, need, lane, tbase);
       if (got != kNone) {
         my = got;
-        sel = ts.sel_word(P.s0 + got);
+        item_words<MULTI>(P, ts, got, sel, elo);
         c = rank;
       }
     }
@@ -169,7 +193,7 @@ __device__ __forceinline__ void trial_loop(const SharedParams& P, const TrialStr
     bool a0, a1, out;
     uint32_t j0, j1, ball;
     while (true) {
-      const Philox4 x = ts(c, sel);
+      const Philox4 x = item_call<MULTI>(ts, c, sel, elo);
       j0 = __umulhi(x.x, M);
       j1 = __umulhi(x.z, M);
       // branch-free: both gathers always issue (j < M is always a valid index)
@@ -210,18 +234,17 @@ __device__ __forceinline__ void trial_loop(const SharedParams& P, const TrialStr
 // rounds finish some lane, so the hand-out has a fast path: the current chunk covers every
 // idle lane -> one popc and a 32-bit add (selection indices are < K < 2^32); only a chunk
 // boundary takes the general loop (refill / prefetch).
-template <int PATH, int NC>
+template <int PATH, int NC, bool MULTI>
 __device__ __forceinline__ void lane_loop(const SharedParams& P, const TrialStream& ts, uint32_t sbase, Pool pl) {
   const uint32_t M = P.M;
   const uint32_t half = P.max_trials >> 1;
   const uint32_t calls = half + (P.max_trials & 1u);
   const uint32_t lane = threadIdx.x & 31u;
   const uint32_t lt = lanemask_lt();
-  const uint32_t s0 = P.s0;
   int32_t* const idx_out = P.idx;
   uint32_t* const tr_out = P.trials;
   const bool want_tr = tr_out != nullptr;
-  uint32_t my = kNone, sel = 0, c = 0;
+  uint32_t my = kNone, sel = 0, elo = 0, c = 0;
   bool active = false;
   uint32_t need = kFull;  // lanes without a selection
   while (true) {
@@ -231,7 +254,7 @@ __device__ __forceinline__ void lane_loop(const SharedParams& P, const TrialStre
       if (pl.next < pl.end && (uint32_t)pl.end - nx >= n) {  // fast path: the chunk covers all
         if (!active) {
           my = nx + __popc(need & lt);
-          sel = ts.sel_word(s0 + my);
+          item_words<MULTI>(P, ts, my, sel, elo);
           c = 0;
           active = true;
         }
@@ -244,7 +267,7 @@ __device__ __forceinline__ void lane_loop(const SharedParams& P, const TrialStre
           const bool mine = ((need >> lane) & 1u) && r < avail;
           if (mine) {
             my = (uint32_t)pl.next + r;
-            sel = ts.sel_word(s0 + my);
+            item_words<MULTI>(P, ts, my, sel, elo);
             c = 0;
             active = true;
           }
@@ -257,7 +280,7 @@ __device__ __forceinline__ void lane_loop(const SharedParams& P, const TrialStre
     // NC = 1: call c (trials 2c, 2c+1); NC = 2: calls c and c+1 (trials 2c .. 2c+3), decided
     // in canonical order -- half the per-round bookkeeping per call at the price of the
     // second call when the first accepts (used for p <= 1/4, kernel dispatch below)
-    const Philox4 x = ts(c, sel);
+    const Philox4 x = item_call<MULTI>(ts, c, sel, elo);
     const uint32_t j0 = __umulhi(x.x, M);
     const uint32_t j1 = __umulhi(x.z, M);
     const bool r0 = accept<PATH>(x.y, j0, sbase, P.thr, P.group_shift);
@@ -267,7 +290,7 @@ __device__ __forceinline__ void lane_loop(const SharedParams& P, const TrialStre
     bool a2 = false, a3 = false;
     uint32_t j2 = 0, j3 = 0;
     if constexpr (NC == 2) {
-      const Philox4 y = ts(c + 1u, sel);
+      const Philox4 y = item_call<MULTI>(ts, c + 1u, sel, elo);
       j2 = __umulhi(y.x, M);
       j3 = __umulhi(y.z, M);
       a2 = (c + 1u < calls) & accept<PATH>(y.y, j2, sbase, P.thr, P.group_shift);
@@ -288,7 +311,7 @@ __device__ __forceinline__ void lane_loop(const SharedParams& P, const TrialStre
 // Whole-warp teams (g = 32): the warp works its selections one after another, 64 trials
 // per round, like the matrix kernel -- no per-round team bookkeeping, ~15 instructions of
 // overhead per selection (pool refill by lane 0 once per `grab` selections).
-template <int PATH>
+template <int PATH, bool MULTI>
 __device__ __forceinline__ void warp_loop(const SharedParams& P, const TrialStream& ts, uint32_t sbase, Pool pl) {
   const uint32_t M = P.M;
   const uint32_t half = P.max_trials >> 1;
@@ -297,12 +320,13 @@ __device__ __forceinline__ void warp_loop(const SharedParams& P, const TrialStre
   while (!pl.exhausted) {
     if (pl.next >= pl.end && !pl.refill(lane)) break;
     const uint32_t my = (uint32_t)pl.next++;
-    const uint32_t sel = ts.sel_word(P.s0 + my);
+    uint32_t sel, elo;
+    item_words<MULTI>(P, ts, my, sel, elo);
     int32_t id = -1;
     uint32_t tr = P.max_trials;
     for (uint32_t c0 = 0; c0 < calls; c0 += 32u) {
       const uint32_t c = c0 + lane;
-      const Philox4 x = ts(c, sel);
+      const Philox4 x = item_call<MULTI>(ts, c, sel, elo);
       const uint32_t j0 = __umulhi(x.x, M);
       const uint32_t j1 = __umulhi(x.z, M);
       const bool r0 = accept<PATH>(x.y, j0, sbase, P.thr, P.group_shift);
@@ -368,7 +392,7 @@ __device__ __forceinline__ uint32_t choose_team(float p, uint32_t K, uint32_t nw
   return best;
 }
 
-template <int PATH>
+template <int PATH, bool MULTI>
 __global__ void __launch_bounds__(1024, 1) select_shared_kernel(const SharedParams P) {
   extern __shared__ __align__(16) unsigned char smem[];
   __shared__ uint64_t stage_bar;
@@ -403,7 +427,9 @@ __global__ void __launch_bounds__(1024, 1) select_shared_kernel(const SharedPara
       if (P.trials) P.trials[s] = 0u;
       if (P.tau) P.tau[s] = invalid ? __uint_as_float(0x7fc00000u) : __uint_as_float(kInfBits);
     } else if (P.tau) {
-      P.tau[s] = __fdiv_rn(neg_log_u1(P.seed_lo, P.seed_hi, P.s0 + s, P.epoch), st.a0f);
+      uint32_t e = 0, sl = s;
+      if constexpr (MULTI) split_item(s, P.Ksel, P.kinv, e, sl);
+      P.tau[s] = __fdiv_rn(neg_log_u1(P.seed_lo, P.seed_hi, P.s0 + sl, P.epoch + e), st.a0f);
     }
   }
   __syncthreads();        // publishes the barrier's initialisation and s_g
@@ -432,32 +458,37 @@ __global__ void __launch_bounds__(1024, 1) select_shared_kernel(const SharedPara
     // two calls per round exactly where choose_team priced them (1/128 <= p <= 1/4); a
     // forced g = 1 (GPUAR_TEAM) outside that range runs the one-call loop
     if (st.p <= 0.25f && st.p >= 1.0f / 128.0f)
-      lane_loop<PATH, 2>(P, ts, sbase, pl);
+      lane_loop<PATH, 2, MULTI>(P, ts, sbase, pl);
     else
-      lane_loop<PATH, 1>(P, ts, sbase, pl);
+      lane_loop<PATH, 1, MULTI>(P, ts, sbase, pl);
   }
   else if (g == 32u)
-    warp_loop<PATH>(P, ts, sbase, pl);
+    warp_loop<PATH, MULTI>(P, ts, sbase, pl);
   else
-    trial_loop<PATH>(P, ts, sbase, g, pl);
+    trial_loop<PATH, MULTI>(P, ts, sbase, g, pl);
 }
 
 template <int PATH>
 void set_limit(int bytes) {
-  set_max_dynamic_smem(select_shared_kernel<PATH>, bytes);
+  set_max_dynamic_smem(select_shared_kernel<PATH, false>, bytes);
+  set_max_dynamic_smem(select_shared_kernel<PATH, true>, bytes);
 }
 
 }  // namespace
 
 cudaError_t launch_select_shared(const SharedParams& p, int path, int grid, int block, cudaStream_t st, bool pdl) {
   const size_t sh = p.smem_bytes;
+  const bool multi = p.n_epochs > 1u;
   switch (path) {
     case kPathSmemF32:
-      return launch_pdl(select_shared_kernel<kPathSmemF32>, grid, block, sh, st, pdl, p);
+      return multi ? launch_pdl(select_shared_kernel<kPathSmemF32, true>, grid, block, sh, st, pdl, p)
+                   : launch_pdl(select_shared_kernel<kPathSmemF32, false>, grid, block, sh, st, pdl, p);
     case kPathSmemBf16:
-      return launch_pdl(select_shared_kernel<kPathSmemBf16>, grid, block, sh, st, pdl, p);
+      return multi ? launch_pdl(select_shared_kernel<kPathSmemBf16, true>, grid, block, sh, st, pdl, p)
+                   : launch_pdl(select_shared_kernel<kPathSmemBf16, false>, grid, block, sh, st, pdl, p);
     case kPathSmemGroup:
-      return launch_pdl(select_shared_kernel<kPathSmemGroup>, grid, block, sh, st, pdl, p);
+      return multi ? launch_pdl(select_shared_kernel<kPathSmemGroup, true>, grid, block, sh, st, pdl, p)
+                   : launch_pdl(select_shared_kernel<kPathSmemGroup, false>, grid, block, sh, st, pdl, p);
     default:
       return cudaErrorInvalidValue;
   }
@@ -467,11 +498,11 @@ int select_shared_blocks_per_sm(int path, int block, size_t smem) {
   int n = 0;
   cudaError_t e = cudaErrorInvalidValue;
   if (path == kPathSmemF32)
-    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, select_shared_kernel<kPathSmemF32>, block, smem);
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, select_shared_kernel<kPathSmemF32, false>, block, smem);
   else if (path == kPathSmemBf16)
-    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, select_shared_kernel<kPathSmemBf16>, block, smem);
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, select_shared_kernel<kPathSmemBf16, false>, block, smem);
   else if (path == kPathSmemGroup)
-    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, select_shared_kernel<kPathSmemGroup>, block, smem);
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, select_shared_kernel<kPathSmemGroup, false>, block, smem);
   return e == cudaSuccess ? n : 0;
 }
 

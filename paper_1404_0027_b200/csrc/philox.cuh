@@ -83,6 +83,21 @@ struct TrialStream {
   // per-selection constant of round 1
   __device__ __forceinline__ uint32_t sel_word(uint32_t s) const { return e_hi_k0 ^ s; }
 
+  // both round-1 constants of selection s at another epoch (multi-epoch launches): the
+  // per-selection word and lo(M1*epoch), which call() takes instead of the member e_lo
+  __device__ __forceinline__ void words(uint32_t epoch, uint32_t s, uint32_t& sel, uint32_t& elo) const {
+    const uint64_t p1 = (uint64_t)kPhiloxM1 * epoch;
+    sel = (uint32_t)(p1 >> 32) ^ rk0[0] ^ s;
+    elo = (uint32_t)p1;
+  }
+  __device__ __forceinline__ Philox4 call(uint32_t c, uint32_t sel, uint32_t elo) const {
+    const uint64_t p0 = (uint64_t)kPhiloxM0 * c;
+    uint32_t c0 = sel, c1 = elo, c2 = (uint32_t)(p0 >> 32) ^ k1_tag, c3 = (uint32_t)p0;
+#pragma unroll
+    for (int r = 1; r < 10; ++r) philox_round(c0, c1, c2, c3, rk0[r], rk1[r]);
+    return Philox4{c0, c1, c2, c3};
+  }
+
   __device__ __forceinline__ Philox4 operator()(uint32_t c, uint32_t sel) const { return with_tag(c, sel, k1_tag); }
 
   // same stream family with another tag: k1t = seed_hi ^ tag

@@ -188,6 +188,28 @@ class Selector:
             check(st, "gpuar_select")
         return idx, tau, trials
 
+    def select_epochs(self, n_epochs: int, K: int | None = None, out: tuple | None = None,
+                      with_tau: bool = True, with_trials: bool = True):
+        """gpuar_select_epochs -> (idx, tau, trials) of shape (n_epochs, K): n_epochs
+        consecutive selects in one call (one launch for a shared vector, classic rule)."""
+        K = (self._rows if self._rows > 1 else self.K) if K is None else int(K)
+        n = int(n_epochs)
+        if out is None:
+            idx = torch.empty((n, K), dtype=torch.int32, device=self.device)
+            tau = torch.empty((n, K), dtype=torch.float32, device=self.device) if with_tau else None
+            trials = torch.empty((n, K), dtype=torch.int32, device=self.device) if with_trials else None
+        else:
+            idx, tau, trials = out
+        _check_buf(idx, n * K, torch.int32, self.device, "idx")
+        _check_buf(tau, n * K, torch.float32, self.device, "tau", optional=True)
+        _check_buf(trials, n * K, torch.int32, self.device, "trials", optional=True)
+        self._stream()
+        st = self._lib.gpuar_select_epochs(self._h, K, n, idx.data_ptr(), None if tau is None else tau.data_ptr(),
+                                           None if trials is None else trials.data_ptr())
+        if st:
+            check(st, "gpuar_select_epochs")
+        return idx, tau, trials
+
     def select_host(self, alpha: np.ndarray | torch.Tensor, K: int | None = None, out: tuple | None = None):
         """gpuar_select_host: host (ideally pinned) propensities in, host outputs out."""
         a = alpha if isinstance(alpha, torch.Tensor) else torch.from_numpy(np.ascontiguousarray(alpha, np.float32))

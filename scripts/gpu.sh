@@ -10,7 +10,7 @@
 #   ubench [dir]                      trial-round / Philox instruction-mix microbenchmark (scripts/ubench)
 #   ncu <name> <kernel-regex> <bench args...>
 #                                     one `ncu --set full` capture of the first matching launch after
-#                                     warm-up -> prof_<name>.ncu-rep (+ summary via scripts/ncu_summary.py)
+#                                     warm-up -> prof_<name>.ncu-rep (summarise here: scripts/ncu_summary.py)
 #   launches <name> <bench args...>   ncu launch list (gpu__time_duration, clocks unlocked) -> launches_<name>.csv
 #   ab <dir> "<bench args>|<label>" ...
 #                                     interleaved A/B: lib/exp_base.so (scripts/build_head.sh base) vs
@@ -72,7 +72,6 @@ ncu)
   name=$1; kre=$2; shift 2
   timeout 900 ncu --set full --clock-control none --import-source on -k regex:"$kre" -s 3 -c 1 \
     -o gpurun_out/prof_$name python bench.py "$@" --steps 2 --warmup 3 --no-cpu --no-e2e --no-it > gpurun_out/ncu_$name.log 2>&1
-  python scripts/ncu_summary.py gpurun_out/prof_$name.ncu-rep > gpurun_out/prof_$name.md 2>&1
   tail -5 gpurun_out/ncu_$name.log ;;
 launches)
   name=$1; shift
