@@ -658,12 +658,35 @@ def run_gpuar(args, w, rank, world, local_rank):
         e1.record(stream)
         e1.synchronize()
         rs_gbs = K * 4 * M / (e0.elapsed_time(e1) / n_rs * 1e-3) / 1e9
+        # ... and the same stream sustained (>= sustain_s, power-capped like `sustained`): the
+        # ceiling the sustained selection rate is compared with
+        rs_sus = None
+        if sustained:
+            n_rs2 = max(20, int(args.sustain_s * 1e3 / max(e0.elapsed_time(e1) / n_rs, 1e-3)))
+            with ClockSampler(local_rank) as clk3:
+                clk3.wait_first()
+                t3 = time.perf_counter()
+                e0.record(stream)
+                for _ in range(n_rs2):
+                    sel.row_stats()
+                e1.record(stream)
+                e1.synchronize()
+                t4 = time.perf_counter()
+                time.sleep(0.06)
+                clk3.mark(t3, t4)
+            rs_sus = {"gbs": K * 4 * M / (e0.elapsed_time(e1) / n_rs2 * 1e-3) / 1e9, "launches": n_rs2,
+                      "clocks": clk3.summary()}
         roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                     "traffic": traffic, "peak_source": peaks["_source"] + " hbm_gbs (copy)",
                     "bytes_per_selection": 4 * M + 12, "frac_of_8TBs": achieved / 8000.0,
-                    "row_stats_stream_gbs": rs_gbs, "per": "rank 0's launches (CUDA events on its stream)"}
+                    "row_stats_stream_gbs": rs_gbs, "row_stats_stream_sustained": rs_sus,
+                    "per": "rank 0's launches (CUDA events on its stream)"}
         if sustained:
             sustained["roofline_frac"] = K * (4 * M + 12) / (sus_ms_rank / sustained["steps"] * 1e-3) / 1e9 / peak
+            if rs_sus:
+                # selection bytes/s over the no-trials stream's bytes/s, both sustained
+                sustained["frac_of_row_stats_stream"] = (K * 4 * M / (sus_ms_rank / sustained["steps"] * 1e-3) / 1e9
+                                                         / rs_sus["gbs"])
     else:
         achieved = calls / (ms_step * 1e-3) / 1e9
         mhz = float(peaks.get("sm_max_mhz", 1965.0))

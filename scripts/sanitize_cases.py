@@ -92,6 +92,18 @@ def main():
         sel.sync()
         for e, o in enumerate(outs):
             check(o[0].cpu().numpy(), oracle.ar_select(a, K, seed=SEED, epoch=e, nthreads=8)["idx"], f"shared team {sel.last_team}")
+    # multi-epoch launches (gpuar_select_epochs) on every loop: equal to consecutive selects
+    for a in (synth.uniform(1000), synth.exponential(10_000), synth.pareto(1000), synth.yeast_like(),
+              synth.exponential(70_000)):
+        K = 3000
+        s1, s2 = Selector(a.size, K, SEED), Selector(a.size, K, SEED)
+        for s_ in (s1, s2):
+            s_.set_propensities(torch.from_numpy(a).cuda())
+        ie, _, _ = s1.select_epochs(5, K)
+        seq = [s2.select(K)[0] for _ in range(5)]
+        s1.sync()
+        s2.sync()
+        check(ie.cpu().numpy(), torch.stack(seq).cpu().numpy(), f"select_epochs {a.size}")
     for env in ({"GPUAR_TEAM": "16"}, {"GPUAR_TEAM": "8", "GPUAR_NO_PDL": "1", "GPUAR_SH_BLOCK": "256"}):
         os.environ.update(env)
         a = synth.pareto(1000)

@@ -146,3 +146,35 @@ def test_it_rows_law():
     idx = _run(host, "it")[0]
     h = np.bincount(idx, minlength=4)
     assert oracle.chi2_pvalue(h, oracle.exact_law(a))[1] > 0.001
+
+
+@pytest.mark.slow
+def test_it_rows_c4_full_size_sampled():
+    """Both IT forms at c4's full size (K = 2^20, M = 1029, generated in HBM by libsynth), as
+    bench.py's it_comparison runs them; oracle on sampled rows (first and last 2048, every
+    997th); every row's pick must be an enabled reaction."""
+    import synth.gpu as sg
+    from paper_1404_0027_b200 import Selector
+    M, K = synth.YEAST_M, 1 << 20
+    rates = synth.yeast_rates(M)
+    mat = torch.empty((K, M), dtype=torch.float32, device="cuda")
+    sg.fill_rows(mat, torch.from_numpy(rates).cuda(), synth.GEN_SEED, 0)
+    rows = np.unique(np.concatenate([np.arange(2048), np.arange(K - 2048, K), np.arange(0, K, 997)]))
+    splits = np.nonzero(np.diff(rows) != 1)[0] + 1
+    refs = {}
+    for run in np.split(rows, splits):
+        h = synth.rows(rates, synth.GEN_SEED, int(run[0]), run.size)
+        refs[int(run[0])] = (run, oracle.it_select(h, run.size, seed=SEED, epoch=2, s0=int(run[0]), nthreads=8))
+    for rule in ("it", "it_scan"):
+        sel = Selector(M, K, SEED)
+        sel.set_rule(rule)
+        sel.epoch = 2
+        sel.set_propensities(mat)
+        idx, tau, trials = sel.select(K)
+        sel.sync()
+        gi = idx.cpu().numpy()
+        for run, ref in refs.values():
+            np.testing.assert_array_equal(gi[run], ref)
+        assert (gi >= 0).all() and (trials.cpu().numpy() == 1).all()
+        picked = mat.gather(1, idx.long().unsqueeze(1)).squeeze(1)
+        assert bool((picked > 0).all())
