@@ -623,8 +623,10 @@ def run_gpuar(args, w, rank, world, local_rank):
     # vector in ONE launch, bit-identical to n calls -- an SSA driver keeping the vector for n
     # steps.  Amortises the per-launch ramp, staging and drain; reported beside `value`.
     multi = None
-    if w["kind"] == "shared" and w["rule"] == "classic" and args.epochs != 1:
-        n_ep = args.epochs if args.epochs > 1 else max(2, min(256, (1 << 20) // K))
+    # (auto: n K ~ 2^24 selections per launch, up to 256 epochs; skipped for calls of >= 10 ms,
+    # which have no launch overhead to amortise)
+    if w["kind"] == "shared" and w["rule"] == "classic" and args.epochs != 1 and (args.epochs > 1 or ms_step < 10.0):
+        n_ep = args.epochs if args.epochs > 1 else max(2, min(256, (1 << 24) // K))
         o_ep = tuple(torch.empty((n_ep, K), dtype=dt, device=device) for dt in (torch.int32, torch.float32, torch.int32))
         for _ in range(3):
             sel.select_epochs(n_ep, K, out=o_ep)

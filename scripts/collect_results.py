@@ -46,6 +46,21 @@ def main():
     print("|---|---|---|---|---|---|---|---|---|---|---|---|")
     for row in rows:
         print("| " + " | ".join(str(x) for x in row) + " |")
+    # round-2 sub-records: sustained (power-capped), multi-epoch launches, IT beside AR
+    print()
+    print("| run | sustained value | sustained SM MHz | multi-epoch value (epochs/launch, frac) | IT prefix+search | IT linear scan | AR / IT scan |")
+    print("|---|---|---|---|---|---|---|")
+    for p in sorted(glob.glob(os.path.join(d, "*.json"))):
+        r = load(p)
+        if not r or "roofline" not in r:
+            continue
+        sus = r.get("sustained") or {}
+        me = r.get("multi_epoch") or {}
+        it = r.get("it_comparison") or {}
+        print(f"| {os.path.basename(p)[:-5]} | {fmt(sus.get('value'))} | {(sus.get('clocks') or {}).get('sm_mhz', '—')} | "
+              f"{fmt(me.get('value'))}" + (f" ({me.get('epochs_per_launch')}, {fmt(me.get('frac'))})" if me else "") +
+              f" | {fmt((it.get('it') or {}).get('value'))} | {fmt((it.get('it_scan') or {}).get('value'))} | "
+              f"{fmt(it.get('ar_over_it_scan'))} |")
 
 
 if __name__ == "__main__":
