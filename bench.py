@@ -97,6 +97,8 @@ def parse():
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-it", action="store_true", help="skip the inverse-transform comparison (matrix configs)")
+    ap.add_argument("--no-stream-ceiling", action="store_true",
+                    help="skip the row-stats stream diagnostics (matrix configs; ncu launch lists)")
     ap.add_argument("--epochs", type=int, default=0,
                     help="epochs per gpuar_select_epochs launch for the multi_epoch record (0: auto, 1: skip)")
     ap.add_argument("--no-cpu", action="store_true")
@@ -652,18 +654,19 @@ def run_gpuar(args, w, rank, world, local_rank):
         # diagnostic: the same row pipeline streaming the matrix with only the alpha_max /
         # alpha_0 reduction (gpuar_row_stats, no trials) -- what the pipeline itself can read
         e0, e1 = ev_pair()
-        sel.row_stats()
-        n_rs = 20
+        n_rs = 0 if args.no_stream_ceiling else 20
+        if n_rs:
+            sel.row_stats()
         e0.record(stream)
         for _ in range(n_rs):
             sel.row_stats()
         e1.record(stream)
         e1.synchronize()
-        rs_gbs = K * 4 * M / (e0.elapsed_time(e1) / n_rs * 1e-3) / 1e9
+        rs_gbs = K * 4 * M / (e0.elapsed_time(e1) / n_rs * 1e-3) / 1e9 if n_rs else None
         # ... and the same stream sustained (>= sustain_s, power-capped like `sustained`): the
         # ceiling the sustained selection rate is compared with
         rs_sus = None
-        if sustained:
+        if sustained and n_rs:
             n_rs2 = max(20, int(args.sustain_s * 1e3 / max(e0.elapsed_time(e1) / n_rs, 1e-3)))
             with ClockSampler(local_rank) as clk3:
                 clk3.wait_first()

@@ -46,7 +46,7 @@ final)
   timeout 600 python bench.py --config s1 --steps 20 > $out/s1.json 2>&1
   timeout 120 python scripts/philox_peak.py > $out/philox_peak.txt 2>&1
   timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $out/launches_c4.csv \
-    python bench.py --steps 5 --warmup 3 --no-e2e --no-cpu --no-it > $out/launches_c4.log 2>&1
+    python bench.py --steps 5 --warmup 3 --no-e2e --no-cpu --no-it --sustain-s 0 --epochs 1 --no-stream-ceiling > $out/launches_c4.log 2>&1
   python scripts/collect_results.py $out > $out/results.md ;;
 sanitize)
   out=gpurun_out/san; mkdir -p $out; rm -f $out/summary.txt
@@ -71,12 +71,12 @@ ubench)
 ncu)
   name=$1; kre=$2; shift 2
   timeout 900 ncu --set full --clock-control none --import-source on -k regex:"$kre" -s 3 -c 1 \
-    -o gpurun_out/prof_$name python bench.py "$@" --steps 2 --warmup 3 --no-cpu --no-e2e --no-it > gpurun_out/ncu_$name.log 2>&1
+    -o gpurun_out/prof_$name python bench.py "$@" --steps 2 --warmup 3 --no-cpu --no-e2e --no-it --sustain-s 0 --epochs 1 --no-stream-ceiling > gpurun_out/ncu_$name.log 2>&1
   tail -5 gpurun_out/ncu_$name.log ;;
 launches)
   name=$1; shift
   timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_$name.csv \
-    python bench.py "$@" --steps 5 --warmup 3 --no-cpu --no-e2e --no-it > gpurun_out/launches_$name.log 2>&1
+    python bench.py "$@" --steps 5 --warmup 3 --no-cpu --no-e2e --no-it --sustain-s 0 --epochs 1 --no-stream-ceiling > gpurun_out/launches_$name.log 2>&1
   tail -2 gpurun_out/launches_$name.log ;;
 ab)
   out=gpurun_out/$1; shift; mkdir -p $out
