@@ -33,29 +33,41 @@ namespace {
 
 // Trials of one row by one warp: round t = Philox calls [32t, 32t+32), lane l -> call
 // 32t + l -> trials 2c, 2c+1; the ballot's lowest lane (even trial first) is the first
-// accept in canonical order (R6).
+// accept in canonical order (R6).  Rounds whose 64 trials all lie below max_trials
+// (every round a selection reaches at the default cap) skip the cap tests: c0 + 31 < half.
+template <bool FOLD, bool CAP, class Stream>
+__device__ __forceinline__ bool row_round(const Stream& ts, uint32_t c0, uint32_t sel, uint32_t row_s, uint32_t M,
+                                          float amax, float amax_s, uint32_t half, uint32_t calls, uint32_t lane,
+                                          int32_t& id, uint32_t& tr) {
+  const uint32_t c = c0 + lane;
+  const Philox4 x = ts(c, sel);
+  const uint32_t j0 = __umulhi(x.x, M);
+  const uint32_t j1 = __umulhi(x.z, M);
+  const float v0 = lds_f32(row_s + 4u * j0);
+  const float v1 = lds_f32(row_s + 4u * j1);
+  const bool a0 = (!CAP || c < calls) & (scaled_u<FOLD>(x.y, amax, amax_s) < v0);
+  const bool a1 = (!CAP || c < half) & (scaled_u<FOLD>(x.w, amax, amax_s) < v1);
+  const uint32_t b = __ballot_sync(kFull, a0 || a1);
+  if (b != 0u) {
+    const uint32_t w = __ffs(b) - 1;
+    id = (int32_t)__shfl_sync(kFull, a0 ? j0 : j1, w);
+    tr = __shfl_sync(kFull, a0 ? 2u * c + 1u : 2u * c + 2u, w);
+    return true;
+  }
+  return false;
+}
+
 template <bool FOLD, class Stream>
 __device__ __forceinline__ void row_trials(const Stream& ts, uint32_t sel, uint32_t row_s, uint32_t M,
                                            float amax, uint32_t half, uint32_t calls, uint32_t lane, int32_t& id,
                                            uint32_t& tr) {
   const float amax_s = __fmul_rn(amax, 0x1p-24f);
-  for (uint32_t c0 = 0; c0 < calls; c0 += 32u) {
-    const uint32_t c = c0 + lane;
-    const Philox4 x = ts(c, sel);
-    const uint32_t j0 = __umulhi(x.x, M);
-    const uint32_t j1 = __umulhi(x.z, M);
-    const float v0 = lds_f32(row_s + 4u * j0);
-    const float v1 = lds_f32(row_s + 4u * j1);
-    const bool a0 = (c < calls) & (scaled_u<FOLD>(x.y, amax, amax_s) < v0);
-    const bool a1 = (c < half) & (scaled_u<FOLD>(x.w, amax, amax_s) < v1);
-    const uint32_t b = __ballot_sync(kFull, a0 || a1);
-    if (b != 0u) {
-      const uint32_t w = __ffs(b) - 1;
-      id = (int32_t)__shfl_sync(kFull, a0 ? j0 : j1, w);
-      tr = __shfl_sync(kFull, a0 ? 2u * c + 1u : 2u * c + 2u, w);
-      return;
-    }
-  }
+  const uint32_t free_end = half & ~31u;  // c0 < free_end (c0 a multiple of 32) <=> c0 + 31 < half
+  uint32_t c0 = 0;
+  for (; c0 < free_end; c0 += 32u)
+    if (row_round<FOLD, false>(ts, c0, sel, row_s, M, amax, amax_s, half, calls, lane, id, tr)) return;
+  for (; c0 < calls; c0 += 32u)
+    if (row_round<FOLD, true>(ts, c0, sel, row_s, M, amax, amax_s, half, calls, lane, id, tr)) return;
 }
 
 // N Philox calls' reactions 4c_i..4c_i+3 (FULL: all < M, else bounds-tested), calls in

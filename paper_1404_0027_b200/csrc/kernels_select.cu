@@ -17,6 +17,7 @@
 //    ahead): work stealing, so geometric trial counts leave no long tail;
 //  * tau is a separate, fully coalesced grid-stride phase.
 #include <algorithm>
+#include <type_traits>
 
 #include "gpuar_internal.cuh"
 #include "philox.cuh"
@@ -316,6 +317,7 @@ __device__ __forceinline__ void warp_loop(const SharedParams& P, const TrialStre
   const uint32_t M = P.M;
   const uint32_t half = P.max_trials >> 1;
   const uint32_t calls = half + (P.max_trials & 1u);
+  const uint32_t free_end = half & ~31u;  // rounds starting below it need no cap test
   const uint32_t lane = threadIdx.x & 31u;
   while (!pl.exhausted) {
     if (pl.next >= pl.end && !pl.refill(lane)) break;
@@ -324,23 +326,33 @@ __device__ __forceinline__ void warp_loop(const SharedParams& P, const TrialStre
     item_words<MULTI>(P, ts, my, sel, elo);
     int32_t id = -1;
     uint32_t tr = P.max_trials;
-    for (uint32_t c0 = 0; c0 < calls; c0 += 32u) {
+    // one round: calls [c0, c0 + 32); CAP: test the trials against max_trials (only rounds
+    // reaching past half = floor(max_trials / 2) need it)
+    auto round = [&](uint32_t c0, auto cap) -> bool {
       const uint32_t c = c0 + lane;
       const Philox4 x = item_call<MULTI>(ts, c, sel, elo);
       const uint32_t j0 = __umulhi(x.x, M);
       const uint32_t j1 = __umulhi(x.z, M);
       const bool r0 = accept<PATH>(x.y, j0, sbase, P.thr, P.group_shift);
       const bool r1 = accept<PATH>(x.w, j1, sbase, P.thr, P.group_shift);
-      const bool a0 = (c < calls) & r0;
-      const bool a1 = (c < half) & r1;
+      const bool a0 = (!decltype(cap)::value || c < calls) & r0;
+      const bool a1 = (!decltype(cap)::value || c < half) & r1;
       const uint32_t b = __ballot_sync(kFull, a0 || a1);
       if (b != 0u) {
         const uint32_t w = __ffs(b) - 1;
         id = (int32_t)__shfl_sync(kFull, a0 ? j0 : j1, w);
         tr = __shfl_sync(kFull, a0 ? 2u * c + 1u : 2u * c + 2u, w);
-        break;
+        return true;
       }
-    }
+      return false;
+    };
+    uint32_t c0 = 0;
+    bool hit = false;
+    for (; c0 < free_end; c0 += 32u)
+      if ((hit = round(c0, std::false_type{}))) break;
+    if (!hit)
+      for (; c0 < calls; c0 += 32u)
+        if (round(c0, std::true_type{})) break;
     if (lane == 0u) {
       P.idx[my] = id;
       if (P.trials) P.trials[my] = tr;

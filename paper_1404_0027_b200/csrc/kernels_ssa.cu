@@ -35,25 +35,37 @@ __device__ __forceinline__ float propensity(uint32_t xs, const int4 d) {
   return __fmul_rn(__fmul_rn(__fmul_rn(__int_as_float(d.z), (float)x0), (float)x1), h);
 }
 
+template <bool FOLD, bool CAP>
+__device__ __forceinline__ bool ssa_round(const TrialStream& ts, uint32_t c0, uint32_t sel, uint32_t row_s, uint32_t M,
+                                          float amax, float amax_s, uint32_t half, uint32_t calls, uint32_t lane,
+                                          int32_t& id) {
+  const uint32_t c = c0 + lane;
+  const Philox4 x = ts(c, sel);
+  const uint32_t j0 = __umulhi(x.x, M);
+  const uint32_t j1 = __umulhi(x.z, M);
+  const float v0 = lds_f32(row_s + 4u * j0);
+  const float v1 = lds_f32(row_s + 4u * j1);
+  const bool a0 = (!CAP || c < calls) & (scaled_u<FOLD>(x.y, amax, amax_s) < v0);
+  const bool a1 = (!CAP || c < half) & (scaled_u<FOLD>(x.w, amax, amax_s) < v1);
+  const uint32_t b = __ballot_sync(kFull, a0 || a1);
+  if (b != 0u) {
+    id = (int32_t)__shfl_sync(kFull, a0 ? j0 : j1, __ffs(b) - 1);
+    return true;
+  }
+  return false;
+}
+
 template <bool FOLD>
 __device__ __forceinline__ void ssa_trials(const TrialStream& ts, uint32_t sel, uint32_t row_s, uint32_t M,
                                            float amax, uint32_t half, uint32_t calls, uint32_t lane, int32_t& id) {
   const float amax_s = __fmul_rn(amax, 0x1p-24f);
-  for (uint32_t c0 = 0; c0 < calls; c0 += 32u) {
-    const uint32_t c = c0 + lane;
-    const Philox4 x = ts(c, sel);
-    const uint32_t j0 = __umulhi(x.x, M);
-    const uint32_t j1 = __umulhi(x.z, M);
-    const float v0 = lds_f32(row_s + 4u * j0);
-    const float v1 = lds_f32(row_s + 4u * j1);
-    const bool a0 = (c < calls) & (scaled_u<FOLD>(x.y, amax, amax_s) < v0);
-    const bool a1 = (c < half) & (scaled_u<FOLD>(x.w, amax, amax_s) < v1);
-    const uint32_t b = __ballot_sync(kFull, a0 || a1);
-    if (b != 0u) {
-      id = (int32_t)__shfl_sync(kFull, a0 ? j0 : j1, __ffs(b) - 1);
-      return;
-    }
-  }
+  // rounds entirely below max_trials skip the cap tests (c0 + 31 < half), as in row_trials
+  const uint32_t free_end = half & ~31u;
+  uint32_t c0 = 0;
+  for (; c0 < free_end; c0 += 32u)
+    if (ssa_round<FOLD, false>(ts, c0, sel, row_s, M, amax, amax_s, half, calls, lane, id)) return;
+  for (; c0 < calls; c0 += 32u)
+    if (ssa_round<FOLD, true>(ts, c0, sel, row_s, M, amax, amax_s, half, calls, lane, id)) return;
 }
 
 __global__ void __launch_bounds__(768, 1) ssa_kernel(const SsaParams P) {
