@@ -178,3 +178,25 @@ def test_it_rows_c4_full_size_sampled():
         assert (gi >= 0).all() and (trials.cpu().numpy() == 1).all()
         picked = mat.gather(1, idx.long().unsqueeze(1)).squeeze(1)
         assert bool((picked > 0).all())
+
+
+@pytest.mark.parametrize("rule", ["it", "it_scan", "argmin"])
+def test_select_host_rules_on_rows(rule):
+    """gpuar_select_host (the e2e path: chunked H2D, select, D2H on three streams) with the
+    non-classic rules on a matrix spanning three 64 MB host chunks: identical to the device
+    path and (IT) to the oracle."""
+    from paper_1404_0027_b200 import Selector
+    M, K = 1029, 40_000
+    host = synth.rows(synth.yeast_rates(M), synth.GEN_SEED, 0, K)
+    sel = Selector(M, K, SEED)
+    sel.set_rule(rule, 1.0)
+    sel.set_selection_offset(77)
+    hi, ht, htr = sel.select_host(torch.from_numpy(host).pin_memory())
+    sel.epoch = 0
+    sel.set_propensities(torch.from_numpy(host).cuda())
+    di, dt, dtr = sel.select(K)
+    sel.sync()
+    assert torch.equal(hi, di.cpu()) and torch.equal(htr, dtr.cpu())
+    assert torch.equal(ht.view(torch.int32), dt.cpu().view(torch.int32))
+    if rule != "argmin":
+        np.testing.assert_array_equal(hi.numpy(), oracle.it_select(host, K, seed=SEED, s0=77, nthreads=8))
