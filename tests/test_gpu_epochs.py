@@ -98,3 +98,22 @@ def test_epochs_errors():
     sel.set_rule("it_scan")
     with pytest.raises(GpuarError):
         sel.select_epochs(2, 10)
+
+
+def test_c2_multi_epoch_at_bench_config():
+    """c2 (M = 1029 yeast-like, K = 65 536) as bench.py's multi_epoch record launches it: 256
+    epochs in one launch; sampled epochs against the oracle, trials and tau included."""
+    from paper_1404_0027_b200 import Selector
+    a = synth.yeast_like()
+    K, n = 65_536, 256
+    sel = Selector(a.size, K, SEED)
+    sel.set_propensities(torch.from_numpy(a).cuda())
+    sel.epoch = 9
+    idx, tau, tr = sel.select_epochs(n)
+    sel.sync()
+    idx, tau, tr = idx.cpu().numpy(), tau.cpu().numpy(), tr.cpu().numpy().view(np.uint32)
+    for e in (0, 1, 128, 255):
+        ref = oracle.ar_select(a, K, seed=SEED, epoch=9 + e, nthreads=8)
+        np.testing.assert_array_equal(idx[e], ref["idx"])
+        np.testing.assert_array_equal(tr[e], ref["trials"])
+        assert (np.abs(tau[e] - ref["tau_ref"]) / ref["tau_ref"]).max() <= 1e-6
