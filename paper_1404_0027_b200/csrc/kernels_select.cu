@@ -78,64 +78,60 @@ __device__ __forceinline__ Philox4 item_call(const TrialStream& ts, uint32_t c, 
 // stripe holds K/kStripes selections, so stripes finish within ~1/sqrt(K/kStripes) of
 // each other), so each warp makes at most one failing atomic.
 struct Pool {
-  unsigned long long next, end;  // current chunk [next, end)
-  unsigned long long grab, first;
+  uint32_t next, end;            // current chunk [next, end) (selections < K < 2^32)
+  uint32_t hi;                   // end of this warp's stripe
+  uint32_t grab;                 // selections per ticket grab
+  unsigned long long dbase;      // start of the stripe's dynamic part (after the static chunks)
   unsigned long long pending;    // lane 0: ticket of the NEXT chunk, fetched one chunk ahead
   unsigned long long* tickets;   // this launch's ticket set (DevCounters::next[phase])
-  uint32_t K, nwarps, stripe;
+  uint32_t stripe;
   bool exhausted;
 
   // Lane 0 issues the atomic for the chunk after the current one; its latency (~1 us under
   // contention) overlaps the current chunk's work instead of stalling the warp.
   bool ahead;                    // prefetch one chunk ahead (else fetch on demand)
   __device__ __forceinline__ void prefetch(uint32_t lane) {
-    if (lane == 0u) pending = dyn_base(stripe) + atomicAdd(&tickets[stripe], grab);
+    if (lane == 0u) pending = dbase + atomicAdd(&tickets[stripe], (unsigned long long)grab);
   }
   // Move to the prefetched chunk (and prefetch the one after); false when the stripe is done.
   __device__ __forceinline__ bool refill(uint32_t lane) {
     if (!ahead) prefetch(lane);
     const unsigned long long b = __shfl_sync(kFull, pending, 0);
-    const unsigned long long hi = stripe_hi(stripe);
     if (b >= hi) {
       exhausted = true;
       return false;
     }
-    next = b;
-    end = min(b + grab, hi);
+    next = (uint32_t)b;
+    end = next + min(grab, hi - next);
     if (ahead) prefetch(lane);
     return true;
   }
-
-  __device__ __forceinline__ unsigned long long stripe_lo(uint32_t s) const {
-    const unsigned long long sz = ((unsigned long long)K + kStripes - 1) / kStripes;
-    return min((unsigned long long)s * sz, (unsigned long long)K);
-  }
-  __device__ __forceinline__ unsigned long long stripe_hi(uint32_t s) const { return stripe_lo(s + 1); }
-  // start of the dynamic part of stripe s (after its warps' static chunks)
-  __device__ __forceinline__ unsigned long long dyn_base(uint32_t s) const {
-    const unsigned long long nw = (nwarps > s) ? (nwarps - s + kStripes - 1) / kStripes : 0;
-    return stripe_lo(s) + nw * first;
-  }
 };
+
+__device__ __forceinline__ unsigned long long stripe_lo(uint32_t K, uint32_t s) {
+  const unsigned long long sz = ((unsigned long long)K + kStripes - 1) / kStripes;
+  return min((unsigned long long)s * sz, (unsigned long long)K);
+}
 
 __device__ __forceinline__ void pool_init(Pool& pl, uint32_t K, uint32_t nwarps, uint32_t warp_global,
                                           unsigned long long first, unsigned long long grab,
                                           unsigned long long* tickets, bool ahead) {
   pl.ahead = ahead;
   pl.tickets = tickets;
-  pl.K = K;
-  pl.nwarps = nwarps;
-  pl.first = first;
-  pl.grab = grab;
+  pl.grab = (uint32_t)min(grab, (unsigned long long)K);
   pl.stripe = warp_global % kStripes;
-  const unsigned long long hi = pl.stripe_hi(pl.stripe);
-  const unsigned long long lo = pl.stripe_lo(pl.stripe) + (unsigned long long)(warp_global / kStripes) * first;
-  pl.next = min(lo, hi);
-  pl.end = min(lo + first, hi);
+  const unsigned long long hi = stripe_lo(K, pl.stripe + 1);
+  const unsigned long long lo = stripe_lo(K, pl.stripe) + (unsigned long long)(warp_global / kStripes) * first;
+  // start of the dynamic part of the stripe: after all its warps' static chunks
+  const unsigned long long nw = (nwarps > pl.stripe) ? (nwarps - pl.stripe + kStripes - 1) / kStripes : 0;
+  pl.dbase = stripe_lo(K, pl.stripe) + nw * first;
+  pl.hi = (uint32_t)hi;
+  pl.next = (uint32_t)min(lo, hi);
+  pl.end = (uint32_t)min(lo + first, hi);
   // nothing static and no dynamic part left in the stripe: done without touching the ticket
-  pl.exhausted = pl.next >= pl.end && pl.dyn_base(pl.stripe) >= hi;
+  pl.exhausted = pl.next >= pl.end && pl.dbase >= hi;
   pl.pending = ~0ull;
-  if (ahead && pl.dyn_base(pl.stripe) < hi) pl.prefetch(threadIdx.x & 31u);
+  if (ahead && pl.dbase < hi) pl.prefetch(threadIdx.x & 31u);
 }
 
 // Hand idle teams (leader lanes in `need`) the next selections of the warp's pool.
@@ -144,10 +140,10 @@ __device__ __forceinline__ uint32_t pool_take(Pool& pl, uint32_t need, uint32_t 
   uint32_t got = kNone;
   while (need != 0u && !pl.exhausted) {
     if (pl.next >= pl.end && !pl.refill(lane)) break;
-    const uint32_t avail = (uint32_t)(pl.end - pl.next);
+    const uint32_t avail = pl.end - pl.next;
     const uint32_t r = __popc(need & lanemask_lt());
     uint32_t mine = kNone;
-    if (((need >> lane) & 1u) && r < avail) mine = (uint32_t)pl.next + r;
+    if (((need >> lane) & 1u) && r < avail) mine = pl.next + r;
     mine = __shfl_sync(kFull, mine, tbase);
     if (mine != kNone) got = mine;
     pl.next += min((uint32_t)__popc(need), avail);
@@ -235,7 +231,7 @@ __device__ __forceinline__ void trial_loop(const SharedParams& P, const TrialStr
 // rounds finish some lane, so the hand-out has a fast path: the current chunk covers every
 // idle lane -> one popc and a 32-bit add (selection indices are < K < 2^32); only a chunk
 // boundary takes the general loop (refill / prefetch).
-template <int PATH, int NC, bool MULTI>
+template <int PATH, int NC, bool MULTI, bool WANT_TR>
 __device__ __forceinline__ void lane_loop(const SharedParams& P, const TrialStream& ts, uint32_t sbase, Pool pl) {
   const uint32_t M = P.M;
   const uint32_t half = P.max_trials >> 1;
@@ -243,16 +239,15 @@ __device__ __forceinline__ void lane_loop(const SharedParams& P, const TrialStre
   const uint32_t lane = threadIdx.x & 31u;
   const uint32_t lt = lanemask_lt();
   int32_t* const idx_out = P.idx;
-  uint32_t* const tr_out = P.trials;
-  const bool want_tr = tr_out != nullptr;
+  uint32_t* const tr_out = P.trials;  // non-null iff WANT_TR (a compile-time branch per round)
   uint32_t my = kNone, sel = 0, elo = 0, c = 0;
   bool active = false;
   uint32_t need = kFull;  // lanes without a selection
   while (true) {
     if (need != 0u) {  // warp-uniform: hand out selections
       const uint32_t n = __popc(need);
-      const uint32_t nx = (uint32_t)pl.next;
-      if (pl.next < pl.end && (uint32_t)pl.end - nx >= n) {  // fast path: the chunk covers all
+      const uint32_t nx = pl.next;
+      if (pl.end - nx >= n) {  // fast path: the chunk covers all (next <= end always)
         if (!active) {
           my = nx + __popc(need & lt);
           item_words<MULTI>(P, ts, my, sel, elo);
@@ -263,11 +258,11 @@ __device__ __forceinline__ void lane_loop(const SharedParams& P, const TrialStre
       } else {
         while (need != 0u && !pl.exhausted) {
           if (pl.next >= pl.end && !pl.refill(lane)) break;
-          const uint32_t avail = (uint32_t)(pl.end - pl.next);
+          const uint32_t avail = pl.end - pl.next;
           const uint32_t r = __popc(need & lt);
           const bool mine = ((need >> lane) & 1u) && r < avail;
           if (mine) {
-            my = (uint32_t)pl.next + r;
+            my = pl.next + r;
             item_words<MULTI>(P, ts, my, sel, elo);
             c = 0;
             active = true;
@@ -300,7 +295,7 @@ __device__ __forceinline__ void lane_loop(const SharedParams& P, const TrialStre
     const bool done = active & (a0 | a1 | a2 | a3 | (c + (uint32_t)NC >= calls));
     if (done) {
       idx_out[my] = a0 ? (int32_t)j0 : a1 ? (int32_t)j1 : a2 ? (int32_t)j2 : a3 ? (int32_t)j3 : -1;
-      if (want_tr)
+      if constexpr (WANT_TR)
         tr_out[my] = a0 ? 2u * c + 1u : a1 ? 2u * c + 2u : a2 ? 2u * c + 3u : a3 ? 2u * c + 4u : P.max_trials;
       active = false;
     }
@@ -321,7 +316,7 @@ __device__ __forceinline__ void warp_loop(const SharedParams& P, const TrialStre
   const uint32_t lane = threadIdx.x & 31u;
   while (!pl.exhausted) {
     if (pl.next >= pl.end && !pl.refill(lane)) break;
-    const uint32_t my = (uint32_t)pl.next++;
+    const uint32_t my = pl.next++;
     uint32_t sel, elo;
     item_words<MULTI>(P, ts, my, sel, elo);
     int32_t id = -1;
@@ -469,10 +464,18 @@ __global__ void __launch_bounds__(1024, 1) select_shared_kernel(const SharedPara
   if (g == 1u) {
     // two calls per round exactly where choose_team priced them (1/128 <= p <= 1/4); a
     // forced g = 1 (GPUAR_TEAM) outside that range runs the one-call loop
-    if (st.p <= 0.25f && st.p >= 1.0f / 128.0f)
-      lane_loop<PATH, 2, MULTI>(P, ts, sbase, pl);
-    else
-      lane_loop<PATH, 1, MULTI>(P, ts, sbase, pl);
+    const bool two = st.p <= 0.25f && st.p >= 1.0f / 128.0f;
+    if (P.trials) {
+      if (two)
+        lane_loop<PATH, 2, MULTI, true>(P, ts, sbase, pl);
+      else
+        lane_loop<PATH, 1, MULTI, true>(P, ts, sbase, pl);
+    } else {
+      if (two)
+        lane_loop<PATH, 2, MULTI, false>(P, ts, sbase, pl);
+      else
+        lane_loop<PATH, 1, MULTI, false>(P, ts, sbase, pl);
+    }
   }
   else if (g == 32u)
     warp_loop<PATH, MULTI>(P, ts, sbase, pl);
