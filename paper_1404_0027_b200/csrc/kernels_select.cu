@@ -15,7 +15,10 @@
 //  * teams that finish take the next selection from a warp-local pool refilled from one of
 //    64 striped tickets (one 64-bit atomic per `grab` selections, prefetched one chunk
 //    ahead): work stealing, so geometric trial counts leave no long tail;
-//  * tau is a separate, fully coalesced grid-stride phase.
+//  * tau is a separate, fully coalesced grid-stride phase;
+//  * MULTI: one launch works n consecutive selects (gpuar_select_epochs): the work items are
+//    the n*K (epoch, selection) pairs, item q -> selection q mod K at epoch + q / K, output
+//    slot q.
 #include <algorithm>
 #include <type_traits>
 
