@@ -118,7 +118,9 @@ int gpuar_select(gpuar_t h, int64_t K, int32_t *d_idx, float *d_tau, uint32_t *d
  * vector for several steps calls select (§Methods: the selection repeats
  * every time step); other rules and the matrix run one launch per epoch.
  * Errors: as gpuar_select, and EINVAL for n_epochs < 1, n_epochs > 65536 or
- * K * n_epochs >= 2^32. */
+ * K * n_epochs >= 2^32 (nothing enqueued, epoch unchanged).  When one of the per-epoch
+ * launches of the looped case fails, the epoch has advanced by the launches enqueued before
+ * it. */
 int gpuar_select_epochs(gpuar_t h, int64_t K, int64_t n_epochs, int32_t *d_idx, float *d_tau, uint32_t *d_trials);
 
 /* End-to-end variant for HOST buffers: copies h_alpha (rows x ld floats, or M floats
