@@ -67,7 +67,7 @@ CONFIGS = {
     "c5": dict(kind="shared", dist="pareto", M=1_000_000, K=1 << 21, max_trials=1 << 24,
                desc="c5: M=1e6 Pareto(1.5) shared vector, K=2^21 selections per GPU (2^24 at 8 GPUs)"),
     # NEXT-2: the full SSA loop (propensities + selection + state update) on chip
-    "s1": dict(kind="ssa", dist="yeast-network", M=1029, K=1 << 17, inner=16,
+    "s1": dict(kind="ssa", dist="yeast-network", M=1029, N=641, K=1 << 17, inner=16,
                desc="s1: full SSA steps, yeast-like mass-action network (641 species, 1029 reactions), "
                     "K=2^17 realizations per GPU, 16 steps per launch"),
     # NEXT-1: the paper's printed election + argmin rule on its own Table 1 / Fig. 2 workload
@@ -311,6 +311,28 @@ def oracle_rate(w: dict, seconds: float, threads: int, max_rows: int | None = No
     return total_u / total_t, nn, total_t
 
 
+# ----------------------------------------------------------------- the workload's config record
+
+def bench_config(w: dict, args, world: int) -> dict:
+    """The `config` object of the JSON line -- identical for our arm and the reference arm
+    (the driver compares them): the workload and its sizes only."""
+    from paper_1404_0027_b200.dist import shard
+    M = w["M"]
+    if w["kind"] == "ssa":
+        return {"workload": w["desc"], "M": M, "N": w["N"], "K_per_gpu": w["K"], "steps_per_launch": w["inner"]}
+    if args.scaling == "strong":
+        K_total = w["K"]
+        K = shard(K_total, 0, world)[1]          # rank 0's shard, the largest
+        desc = w["desc"].replace("per GPU", "in total")
+    else:
+        K, K_total, desc = w["K"], w["K"] * world, w["desc"]
+    return {"workload": desc, "M": M, "K_per_gpu": K, "K_total": K_total, "dist": w["dist"], "rule": w["rule"],
+            "max_trials": w["max_trials"],
+            "parallelism": f"selections sharded over {world} GPU(s) ({args.scaling} scaling), no data-path collective",
+            "l2": ("inputs larger than L2 (%.2f GB/GPU), no flush" % (K * M * 4 / 1e9)) if w["kind"] == "rows"
+            else "shared vector resident in smem/L2 by design; outputs 12 B/selection"}
+
+
 # ----------------------------------------------------------------- the reference (oracle) arm
 
 def run_reference(args, w, rank, world):
@@ -323,20 +345,21 @@ def run_reference(args, w, rank, world):
     rate, n, _ = oracle_rate(w, min(budget, 2.0), threads, max_rows=(1 << 17) if w["kind"] == "rows" else None)
     n = max(1, min(n, int(rate * budget)))   # one step's sample: ~budget seconds of oracle work
     data = host_sample(w, 0, n)
-    for e in range(args.warmup):
+    warm = max(args.warmup, 3)
+    for e in range(warm):
         oracle_pass(w, data, n, e, threads)
     dt, units = 0.0, 0
     for e in range(args.steps):
-        t, u = oracle_pass(w, data, n, args.warmup + e, threads)
+        t, u = oracle_pass(w, data, n, warm + e, threads)
         dt += t
         units += u
     value = units / dt
     sample = f"{n} of the {w['K']} selections per step ({'rows' if w['kind'] == 'rows' else 'selections'} 0..{n - 1})"
     out = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": unit_of(w), "n_gpus": args.gpus,
-        "steps": args.steps, "warmup": args.warmup, "ms_per_step": dt / args.steps * 1e3,
-        "higher_is_better": True, "scaling": args.scaling, "vs_baseline": None, "dtype": "f32",
-        "data": "synthetic", "config": {"workload": w["desc"], "M": w["M"], "K_per_gpu": w["K"]},
+        "steps": args.steps, "warmup": max(args.warmup, 3), "ms_per_step": dt / args.steps * 1e3,
+        "higher_is_better": True, "scaling": args.scaling if w["kind"] != "ssa" else "weak", "vs_baseline": None,
+        "dtype": "f32", "data": "synthetic", "config": bench_config(w, args, world),
         "cpu_baseline": {"value": value, "unit": unit_of(w), "cores": threads, "kind": "oracle", "sample": sample,
                          "cpu_model": cpu_model()},
         "e2e": {"value": value, "unit": unit_of(w), "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
@@ -815,15 +838,8 @@ def run_gpuar(args, w, rank, world, local_rank):
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": max(args.warmup, 3), "ms_per_step": ms_step, "higher_is_better": True,
             "scaling": args.scaling, "vs_baseline": None, "dtype": "f32", "data": "synthetic (seeded synth/ generators)",
-            "config": {"workload": w["desc"] if args.scaling == "weak" else
-                       w["desc"].replace("per GPU", "in total"),
-                       "M": M, "K_per_gpu": K, "K_total": K_total,
-                       "dist": w["dist"], "rule": w["rule"], "max_trials": w["max_trials"],
-                       "parallelism": f"selections sharded over {world} GPU(s) ({args.scaling} scaling), "
-                                      "no data-path collective",
-                       "l2": ("inputs larger than L2 (%.2f GB/GPU), no flush" % (K * M * 4 / 1e9)) if w["kind"] == "rows"
-                       else "shared vector resident in smem/L2 by design; outputs 12 B/selection",
-                       "path": path},
+            "config": bench_config(w, args, world),
+            "path": path,
             "roofline": roofline,
             "cpu_baseline": cpu,
             "e2e": e2e,
@@ -846,7 +862,7 @@ def run_gpuar(args, w, rank, world, local_rank):
             # its own K20 timing as context
             h = hist[:M].double().cpu().numpy()
             a = alpha.double().cpu().numpy()
-            res["config"]["rule"] = f"argmin (paper's printed election + selection), w={w['w']}"
+            res["rule_desc"] = f"argmin (paper's printed election + selection), w={w['w']}"
             res["paper_context"] = {
                 "mse_vs_normalised_propensities_last_step": float(np.mean((a / a.sum() - h / h.sum()) ** 2)),
                 "paper_k20_sel_per_s": PAPER_K20_SEL_PER_S,
@@ -933,7 +949,7 @@ def run_ssa(args, w, rank, world, local_rank):
                "steps": args.steps, "warmup": max(args.warmup, 3), "ms_per_step": ms / args.steps,
                "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
                "data": "synthetic (seeded synth/ network and initial state)",
-               "config": {"workload": w["desc"], "M": M, "N": inp["N"], "K_per_gpu": K, "steps_per_launch": inner},
+               "config": bench_config(w, args, world),
                "roofline": ssa_roofline(value),
                "cpu_baseline": cpu, "e2e": None, "gpu_launches": args.steps, "clocks": clk.summary(),
                "validation": {"events": events, "events_per_realization_per_launch": events / K / args.steps}}

@@ -33,3 +33,21 @@ def test_reference_arm_other_ranks_exit_quietly():
                           "--steps", "1", "--warmup", "1"], capture_output=True, text=True, timeout=300, cwd=ROOT,
                          env=env)
     assert out.returncode == 0 and out.stdout.strip() == ""
+
+
+def test_reference_config_is_our_arms_config():
+    """The driver compares the two arms' `config` objects: both come from bench_config."""
+    import importlib.util
+    spec = importlib.util.spec_from_file_location("bench_mod", os.path.join(ROOT, "bench.py"))
+    b = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(b)
+    for cfg in ("c1", "c4"):
+        d = _run("--impl", "reference", "--config", cfg, "--steps", "1", "--warmup", "1")
+        old = sys.argv
+        sys.argv = ["bench.py", "--config", cfg]
+        try:
+            args = b.parse()
+        finally:
+            sys.argv = old
+        assert d["config"] == b.bench_config(b.workload(args), args, 1)
+        assert "path" not in d["config"]
