@@ -78,6 +78,7 @@ class Selector:
         self._alpha = None      # keeps the borrowed propensity tensor alive
         self._rows = 0
         self._last_stream = None
+        self._out_ok = None     # key of the last output buffers select() validated
 
     # ----------------------------------------------------------------- lifecycle
     def close(self) -> None:
@@ -176,14 +177,24 @@ class Selector:
             trials = torch.empty(K, dtype=torch.int32, device=self.device) if with_trials else None
         else:
             idx, tau, trials = out
-            _check_buf(idx, K, torch.int32, self.device, "idx")
-            _check_buf(tau, K, torch.float32, self.device, "tau", optional=True)
-            _check_buf(trials, K, torch.int32, self.device, "trials", optional=True)
+        p_idx = idx.data_ptr()
+        p_tau = None if tau is None else tau.data_ptr()
+        p_tr = None if trials is None else trials.data_ptr()
+        if out is not None:
+            # the full checks once per (buffers, K); a repeat call with the same buffers (the
+            # usual SSA / bench loop) only re-keys on their addresses and sizes (~0.3 us
+            # instead of ~2.5 us of Python per call, which a launch-bound c1 call would feel)
+            key = (p_idx, idx.numel(), p_tau, -1 if tau is None else tau.numel(), p_tr,
+                   -1 if trials is None else trials.numel(), K)
+            if key != self._out_ok:
+                _check_buf(idx, K, torch.int32, self.device, "idx")
+                _check_buf(tau, K, torch.float32, self.device, "tau", optional=True)
+                _check_buf(trials, K, torch.int32, self.device, "trials", optional=True)
+                self._out_ok = key
         # (no torch device context: the library switches to the handle's device itself;
         # raw integer addresses: ctypes converts them for the void* parameters)
         self._stream()
-        st = self._lib.gpuar_select(self._h, K, idx.data_ptr(), None if tau is None else tau.data_ptr(),
-                                    None if trials is None else trials.data_ptr())
+        st = self._lib.gpuar_select(self._h, K, p_idx, p_tau, p_tr)
         if st:
             check(st, "gpuar_select")
         return idx, tau, trials
