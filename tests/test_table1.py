@@ -68,9 +68,11 @@ def test_table1_cell_gpu(rule, w):
         assert r["rejected"] == 0        # PAPER.md:581-582 / 633-646
 
 
-def test_recorded_table1_run():
-    """The committed full-protocol run (scripts/table1.py on B200, profiles/table1_r01.json)."""
-    p = os.path.join(ROOT, "profiles", "table1_r01.json")
+@pytest.mark.parametrize("name", ["table1_r01.json", "table1_r02.json"])
+def test_recorded_table1_run(name):
+    """The committed full-protocol runs (scripts/table1.py on B200, profiles/table1_r0*.json:
+    round 1's build and round 2's)."""
+    p = os.path.join(ROOT, "profiles", name)
     if not os.path.exists(p):
         pytest.skip("no recorded Table 1 run")
     rows = json.load(open(p))["rows"]
