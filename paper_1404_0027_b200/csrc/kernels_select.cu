@@ -259,32 +259,7 @@ __device__ __forceinline__ void lane_loop(const SharedParams& P, const TrialStre
         }
         pl.next = nx + n;
       } else {
-        // chunk boundary (every few rounds at high p): if the prefetched chunk covers the
-        // lanes the current one cannot, hand out both in one straight-line step -- the same
-        // assignment the general loop below makes in two iterations and a refill
-        bool done = false;
-        if (pl.ahead && !pl.exhausted) {
-          const unsigned long long b = __shfl_sync(kFull, pl.pending, 0);
-          const uint32_t avail = pl.end - nx;  // < n
-          if (b < pl.hi) {
-            const uint32_t b32 = (uint32_t)b;
-            const uint32_t span = min(pl.grab, pl.hi - b32);  // the prefetched chunk's size
-            if (span >= n - avail) {
-              if (!active) {
-                const uint32_t r = __popc(need & lt);
-                my = r < avail ? nx + r : b32 + (r - avail);
-                item_words<MULTI>(P, ts, my, sel, elo);
-                c = 0;
-                active = true;
-              }
-              pl.next = b32 + (n - avail);
-              pl.end = b32 + span;
-              pl.prefetch(lane);
-              done = true;
-            }
-          }
-        }
-        while (!done && need != 0u && !pl.exhausted) {
+        while (need != 0u && !pl.exhausted) {
           if (pl.next >= pl.end && !pl.refill(lane)) break;
           const uint32_t avail = pl.end - pl.next;
           const uint32_t r = __popc(need & lt);
@@ -298,7 +273,7 @@ __device__ __forceinline__ void lane_loop(const SharedParams& P, const TrialStre
           pl.next += min((uint32_t)__popc(need), avail);
           need &= ~__ballot_sync(kFull, mine);
         }
-        if (!done && pl.exhausted && !__any_sync(kFull, active)) break;
+        if (pl.exhausted && !__any_sync(kFull, active)) break;
       }
     }
     // NC = 1: call c (trials 2c, 2c+1); NC = 2: calls c and c+1 (trials 2c .. 2c+3), decided
