@@ -187,6 +187,17 @@ def test_it_spec_examples_and_partition():
         assert alpha[j] > 0
 
 
+def test_it_prefix_is_the_sequential_binary64_sum():
+    """DESIGN.md R24 (the reading the GPU's IT paths are bit-checked against): C_j is the
+    SEQUENTIAL binary64 prefix.  Hand-worked: alpha = (1, 2^-54, 2^-54, 1).  In binary64
+    1 + 2^-54 rounds back to 1 (2^-54 is below half an ulp of 1, 2^-53), so C = (1, 1, 1, 2)
+    and alpha_0 = 2; for u2 = 1/2 the target is exactly 1 and the first C_j > 1 is j = 3.
+    Exact (or extended-precision, or compensated) prefix sums would cross at j = 1."""
+    a = np.array([1.0, 2.0 ** -54, 2.0 ** -54, 1.0], np.float32)
+    assert oracle.it_one(a, 0.5) == 3
+    assert oracle.it_one(a, 0.4999999) == 0
+
+
 def test_shard_partition_independence():
     # outputs depend only on the global selection index: shards concatenate to the whole
     a = np.array([1, 5, 0.5, 2], np.float32)
