@@ -200,3 +200,15 @@ def test_select_host_rules_on_rows(rule):
     assert torch.equal(ht.view(torch.int32), dt.cpu().view(torch.int32))
     if rule != "argmin":
         np.testing.assert_array_equal(hi.numpy(), oracle.it_select(host, K, seed=SEED, s0=77, nthreads=8))
+
+
+@pytest.mark.parametrize("rule", ["it", "it_scan"])
+def test_it_rows_hand_worked_sequential_rounding(rule):
+    """The oracle pin of tests/test_oracle_pins.py on the GPU: alpha = (1, 2^-54, 2^-54, 1)
+    has binary64 prefix sums (1, 1, 1, 2), so the inverse transform can only pick 0 or 3;
+    exact prefix sums would pick 1 for u2 just above 1/2."""
+    K = 4096
+    host = np.tile(np.array([1.0, 2.0 ** -54, 2.0 ** -54, 1.0], np.float32), (K, 1))
+    idx = _run(host, rule)[0]
+    assert set(np.unique(idx)) == {0, 3}
+    np.testing.assert_array_equal(idx, oracle.it_select(host, K, seed=SEED, nthreads=8))
