@@ -212,3 +212,18 @@ def test_it_rows_hand_worked_sequential_rounding(rule):
     idx = _run(host, rule)[0]
     assert set(np.unique(idx)) == {0, 3}
     np.testing.assert_array_equal(idx, oracle.it_select(host, K, seed=SEED, nthreads=8))
+
+
+def test_it_shared_hand_worked_sequential_rounding():
+    """Same vector as a shared vector: the IT prefix kernel's sequential path (its partial
+    sums round) must give C = (1, 1, 1, 2)."""
+    from paper_1404_0027_b200 import Selector
+    a = np.array([1.0, 2.0 ** -54, 2.0 ** -54, 1.0], np.float32)
+    K = 4096
+    sel = Selector(4, K, SEED)
+    sel.set_rule("it")
+    sel.set_propensities(torch.from_numpy(a).cuda())
+    idx = sel.select(K)[0].cpu().numpy()
+    sel.sync()
+    assert set(np.unique(idx)) == {0, 3}
+    np.testing.assert_array_equal(idx, oracle.it_select(a, K, seed=SEED, nthreads=8))
