@@ -252,3 +252,35 @@ def test_binding_rejects_bad_output_buffers():
     with pytest.raises(ValueError):
         sel.select_host(np.ones((10, a.numel() + 3), np.float32)[:, :a.numel() + 1], K=10)
     sel.sync()
+
+
+# ---------------------------------------------------------------- partition independence, determinism
+
+@pytest.mark.parametrize("G", [2, 4, 8])
+def test_partition_independence_G(G):
+    """SURVEY §4 tier 3: the contiguous shards of G ranks (dist.shard, one handle each, as
+    bench.py runs them) concatenate to the bytes of one G = 1 call -- shared vector and
+    matrix rows, ragged K -- and the same call twice gives the same bytes."""
+    from paper_1404_0027_b200 import Selector
+    from paper_1404_0027_b200.dist import shard
+    K = 10_007
+    a = synth.yeast_like()
+    M = 1029
+    rows = synth.rows(synth.yeast_rates(M), synth.GEN_SEED, 0, K)
+    for kind in ("shared", "rows"):
+        def run(s0, n):
+            sel = Selector(M, n, SEED)
+            sel.set_selection_offset(s0)
+            sel.epoch = 7
+            src = a if kind == "shared" else rows[s0:s0 + n]
+            sel.set_propensities(torch.from_numpy(np.ascontiguousarray(src)).cuda())
+            out = sel.select(n)
+            sel.sync()
+            return [t.cpu().numpy().view(np.uint32) for t in out]
+        whole = run(0, K)
+        again = run(0, K)
+        for x, y in zip(whole, again):
+            np.testing.assert_array_equal(x, y)             # run-to-run determinism
+        parts = [run(*shard(K, r, G)) for r in range(G)]
+        for i in range(3):
+            np.testing.assert_array_equal(np.concatenate([p[i] for p in parts]), whole[i])
