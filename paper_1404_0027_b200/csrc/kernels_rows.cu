@@ -15,6 +15,9 @@
 //    relative, R11), then trials in rounds of 32 Philox calls = 64 trials per
 //    warp with a ballot/__ffs first-accept; -ln(u1) is drawn 32 rows at a time and tau is
 //    formed once per block of rows at the output flush.
+// The same pipeline serves the paper's printed argmin rule (NEXT-1), the inverse transform
+// (NEXT-3: prefix + search, and the linear scan, bit-identical to the oracle's sequential
+// binary64 sums, R24) and gpuar_row_stats, as template modes.
 // Row 4116 bytes is not a multiple of 16, so no 2-D tensor map can describe the matrix;
 // each row's copy covers [floor16(start), ceil16(end)) -- at most 15 extra bytes on
 // each side, always inside 16-byte chunks that hold row data -- EXCEPT where ceil16(end)
