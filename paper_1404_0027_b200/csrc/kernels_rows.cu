@@ -204,6 +204,29 @@ __device__ __forceinline__ int32_t it_scan_from(uint32_t row_s, uint32_t j, uint
   return -1;
 }
 
+// The same linear scan in warp-wide steps of 64 (lane l holds elements j + 2l, j + 2l + 1):
+// one warp scan of the pair sums per 64 elements, then the crossing lane resolves its pair.
+// Half the scan steps of it_scan_from for the same result (all partial sums exact).
+__device__ __forceinline__ int32_t it_scan_pairs(uint32_t row_s, uint32_t M, double target, uint32_t lane) {
+  double C = 0.0;
+  for (uint32_t j = 0; j < M; j += 64u) {
+    const uint32_t k = j + 2u * lane;
+    const double v0 = k < M ? (double)lds_f32(row_s + 4u * k) : 0.0;
+    const double v1 = k + 1u < M ? (double)lds_f32(row_s + 4u * k + 4u) : 0.0;
+    const double pair = __dadd_rn(v0, v1);
+    const double incl = __dadd_rn(C, warp_incl_scan(pair, lane));  // C_{k+1}
+    const uint32_t b = __ballot_sync(kFull, k < M && incl > target);
+    if (b != 0u) {
+      const uint32_t w = (uint32_t)__ffs(b) - 1u;
+      const double first = __dsub_rn(incl, v1);                    // C_k (exact)
+      const bool at0 = __shfl_sync(kFull, first > target ? 1u : 0u, w) != 0u;
+      return (int32_t)(j + 2u * w + (at0 ? 0u : 1u));
+    }
+    C = __shfl_sync(kFull, incl, 31);
+  }
+  return -1;
+}
+
 // The oracle's algorithm verbatim on one lane (rows whose partial sums round): alpha_0 by the
 // sequential sum, then the sequential scan; the last positive j if rounding exhausts it.
 __device__ __noinline__ int32_t it_sequential(uint32_t row_s, uint32_t M, float u2, double& a0) {
@@ -257,7 +280,7 @@ __device__ __forceinline__ void row_it(uint32_t row_s, uint32_t M, uint32_t B, u
   if (ea <= q + 51) {  // warp-uniform
     const double target = __dmul_rn((double)u2, a0);
     if constexpr (SCAN) {
-      id = it_scan_from(row_s, 0u, M, 0.0, target, lane);
+      id = it_scan_pairs(row_s, M, target, lane);
     } else {
       const uint32_t bl = __ballot_sync(kFull, P > target);  // P_31 = a0 > target always
       if (bl != 0u) {
