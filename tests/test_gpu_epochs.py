@@ -117,3 +117,23 @@ def test_c2_multi_epoch_at_bench_config():
         np.testing.assert_array_equal(idx[e], ref["idx"])
         np.testing.assert_array_equal(tr[e], ref["trials"])
         assert (np.abs(tau[e] - ref["tau_ref"]) / ref["tau_ref"]).max() <= 1e-6
+
+
+def test_epochs_with_rejections_and_invalid_vector():
+    """max_trials small enough to reject (trials = max_trials, idx = -1 inside a multi-epoch
+    launch), and an invalid vector: every item of every epoch -1 / NaN and the sticky error."""
+    from paper_1404_0027_b200 import GpuarError, Selector
+    a = synth.pareto(1000)
+    sa, sb = _pair(a, 3000)
+    for s in (sa, sb):
+        s.set_max_trials(5)
+    idx, tr = _compare(sa, sb, 3000, 6, s0=11, epoch=2)
+    assert (idx == -1).any() and (tr[idx == -1] == 5).all()
+    bad = synth.yeast_like().copy()
+    bad[17] = np.nan
+    sel = Selector(bad.size, 500, SEED)
+    sel.set_propensities(torch.from_numpy(bad).cuda())
+    i, t, r = sel.select_epochs(3, 500)
+    with pytest.raises(GpuarError):
+        sel.sync()
+    assert (i.cpu() == -1).all() and torch.isnan(t.cpu()).all() and (r.cpu() == 0).all()
