@@ -46,8 +46,10 @@ __global__ void __launch_bounds__(kStatsThreads) stats_pass1(const float* __rest
                                                              double* part_sum, uint32_t* part_max) {
   __shared__ double sh_sum[kStatsThreads / 32];
   __shared__ uint32_t sh_max[kStatsThreads / 32];
-  pdl_wait();  // programmatic dependent launch (gpuar_internal.cuh)
-  pdl_launch_dependents();
+  // programmatic dependent launch (gpuar_internal.cuh).  The statistics and threshold
+  // kernels do NOT trigger their dependents early: a shared-vector select reads their
+  // outputs before its own wait (kernels_select.cu), so it must start only after they complete.
+  pdl_wait();
   const uint32_t chunk = (M + gridDim.x - 1) / gridDim.x;
   const uint32_t lo = blockIdx.x * chunk;
   const uint32_t hi = min(M, lo + chunk);
@@ -70,8 +72,7 @@ __global__ void __launch_bounds__(kStatsThreads) stats_pass2(const double* part_
                                                              DevCounters* ctr) {
   __shared__ double sh_sum[kStatsThreads / 32];
   __shared__ uint32_t sh_max[kStatsThreads / 32];
-  pdl_wait();
-  pdl_launch_dependents();
+  pdl_wait();  // no early trigger (see stats_pass1)
   double acc = 0.0;
   uint32_t mx = 0;
   for (int i = threadIdx.x; i < nparts; i += kStatsThreads) {
@@ -126,8 +127,7 @@ __device__ __forceinline__ uint32_t accept_threshold(float alpha_j, float amax) 
 //          (x >> 16) > G_g rejects every j of the group; otherwise the exact T_j decides.
 __global__ void thresholds_kernel(const float* __restrict__ alpha, uint32_t M, const DevStats* __restrict__ stats,
                                   uint32_t* thr, uint16_t* pref, uint32_t n_pref, uint32_t group_shift, int path) {
-  pdl_wait();
-  pdl_launch_dependents();
+  pdl_wait();  // no early trigger (see stats_pass1): the select kernels read thr before their wait
   const DevStats st = *stats;
   if (!st.valid) return;  // the select kernels stop on invalid statistics
   const float amax = __uint_as_float(st.amax_bits);

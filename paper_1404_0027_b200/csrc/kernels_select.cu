@@ -408,17 +408,16 @@ __global__ void __launch_bounds__(1024, 1) select_shared_kernel(const SharedPara
   __shared__ uint64_t stage_bar;
   __shared__ uint32_t s_g;
   // Programmatic dependent launch: this grid may be resident before the previous kernel of
-  // the stream has finished (its CTAs fill the SM slots freed by that kernel's tail), so
-  // nothing -- not even a read of the thresholds or statistics -- happens before every
-  // prerequisite grid has completed and its writes are visible.  Then let the next launch
-  // be scheduled as early as possible (it waits here in turn).
-  pdl_wait();
-  pdl_launch_dependents();
-  // the next launch's ticket set (its previous user, launch n - 1, has completed)
-  if (blockIdx.x == 0 && threadIdx.x < kStripes) P.ctr->next[P.phase ^ 1u][threadIdx.x] = 0ull;
+  // the stream has finished (its CTAs fill the SM slots freed by that kernel's tail).  Before
+  // the wait below it touches only what this handle's set_propensities kernels produced --
+  // the thresholds / prefilter and the statistics: those kernels never trigger their
+  // dependents early (kernels_misc.cu), and every other grid of the stream either triggers
+  // only after its own wait (so everything before it has completed) or is a plain launch, so
+  // when this grid starts they have completed and their writes are visible.  Outputs,
+  // tickets and alpha are touched only after the wait.
   // ---- stage the thresholds (path 1) or their prefilter (paths 2, 3) in smem with one bulk async
   // copy per CTA (16-byte hull; the data starts `sbase` bytes into it), issued first so that
-  // it overlaps the statistics load and the tau phase
+  // it overlaps the statistics load, the wait and the tau phase
   const uint32_t sbase = (PATH == kPathSmemF32) ? stage_issue(smem, P.thr, 4u * P.M, &stage_bar)
                                                 : stage_issue(smem, P.prefilter, 2u * P.n_pref, &stage_bar);
   const DevStats st = *P.stats;
@@ -429,6 +428,11 @@ __global__ void __launch_bounds__(1024, 1) select_shared_kernel(const SharedPara
   const uint32_t K = P.K;
   const uint32_t nwarps = nthreads >> 5;
   if (threadIdx.x == 0) s_g = P.team_override ? P.team_override : choose_team(st.p, K, nwarps);  // once per CTA
+  // every prerequisite grid complete; then let the next launch be scheduled early
+  pdl_wait();
+  pdl_launch_dependents();
+  // the next launch's ticket set (its previous user, launch n - 1, has completed)
+  if (blockIdx.x == 0 && threadIdx.x < kStripes) P.ctr->next[P.phase ^ 1u][threadIdx.x] = 0ull;
 
   // ---- phase A: tau for every selection; degenerate / invalid outputs
   for (uint32_t s = tid; s < K; s += nthreads) {

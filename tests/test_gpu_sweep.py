@@ -284,3 +284,27 @@ def test_partition_independence_G(G):
         parts = [run(*shard(K, r, G)) for r in range(G)]
         for i in range(3):
             np.testing.assert_array_equal(np.concatenate([p[i] for p in parts]), whole[i])
+
+
+def test_reregistered_vectors_back_to_back():
+    """The shared-vector select stages the thresholds and reads the statistics before its
+    programmatic-dependent-launch wait: a select enqueued right behind a
+    set_propensities of a DIFFERENT vector (and behind another select) must see the new
+    vector.  Alternate three vectors of one M without any host synchronisation in between."""
+    from paper_1404_0027_b200 import Selector
+    M, K = 1029, 20_000
+    vecs = [synth.yeast_like(), synth.uniform(M), synth.pareto(M)]
+    dev = [torch.from_numpy(np.ascontiguousarray(v)).cuda() for v in vecs]
+    sel = Selector(M, K, SEED)
+    outs, plan = [], []
+    for it in range(24):
+        v = it % 3 if it % 4 else (it + 1) % 3
+        if it == 0 or plan[-1][0] != v:
+            sel.set_propensities(dev[v])
+        plan.append((v, sel.epoch))
+        outs.append(sel.select(K))                 # no sync between calls
+    sel.sync()
+    for (v, e), o in zip(plan, outs):
+        ref = oracle.ar_select(vecs[v], K, seed=SEED, epoch=e, nthreads=8)
+        np.testing.assert_array_equal(o[0].cpu().numpy(), ref["idx"])
+        np.testing.assert_array_equal(o[2].cpu().numpy().view(np.uint32), ref["trials"])
