@@ -750,6 +750,23 @@ def run_gpuar(args, w, rank, world, local_rank):
                # the bound of this number: host<->device bytes per second through PCIe
                "pcie_gbs_per_rank": (h2d + 12 * K) * args.e2e_steps / dt_max / 1e9,
                "timer": "host wall clock around synchronous gpuar_select_host, max over ranks"}
+        if w["kind"] == "rows":
+            # the link's own ceiling: a plain pinned host->device copy of 1 GiB of the same
+            # host buffer (CUDA events), and the e2e loop's fraction of it
+            nb = min(host.numel(), 1 << 28)
+            src = host.view(-1)[:nb]
+            dst = torch.empty(nb, dtype=torch.float32, device=device)
+            dst.copy_(src, non_blocking=True)
+            e0, e1 = ev_pair()
+            e0.record(stream)
+            for _ in range(3):
+                dst.copy_(src, non_blocking=True)
+            e1.record(stream)
+            e1.synchronize()
+            h2d_peak = 3 * 4 * nb / (e0.elapsed_time(e1) * 1e-3) / 1e9
+            e2e["h2d_copy_gbs"] = h2d_peak
+            e2e["pcie_frac"] = e2e["pcie_gbs_per_rank"] / h2d_peak
+            del dst
         del host
         if w["kind"] == "shared":
             sel.set_propensities(alpha)           # select_host registered its own staged copy
