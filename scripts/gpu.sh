@@ -7,6 +7,8 @@
 #                                     the reference arm, the c4 ncu launch list, results.md
 #   sanitize                          compute-sanitizer (memcheck, racecheck, synccheck, initcheck) over
 #                                     scripts/sanitize_cases.py and tests/tail_overread_case.py -> san/
+#                                     (the pool closed compute-sanitizer after r02_compute_sanitizer.md:
+#                                     it now exits 86 at start-up)
 #   ubench [dir]                      trial-round / Philox instruction-mix microbenchmark (scripts/ubench)
 #   ncu <name> <kernel-regex> <bench args...>
 #                                     one `ncu --set full` capture of the first matching launch after
