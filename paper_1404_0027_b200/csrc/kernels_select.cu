@@ -404,11 +404,34 @@ __device__ __forceinline__ uint32_t choose_team(float p, uint32_t K, uint32_t nw
 
 constexpr uint32_t kPreTau = 8;  // tau values per thread computed before the PDL wait
 
+#ifdef GPUAR_TIMELINE
+// Diagnostic build only (scripts/diag_timeline.py; never in libgpuar.so): %globaltimer stamps
+// of the last two launches (slot = epoch & 1): per CTA [entry, after the PDL wait, trials
+// start, %smid], per warp its exit.
+constexpr uint32_t kTlCta = 4u * 1024u, kTlN = kTlCta + 32u * 1024u;
+__device__ unsigned long long g_tl[2][kTlN];
+__device__ __forceinline__ unsigned long long tl_now() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+#define TL_CTA(k, v) \
+  if (threadIdx.x == 0) g_tl[P.epoch & 1u][4u * blockIdx.x + (k)] = (v)
+#endif
+
 template <int PATH, bool MULTI>
 __global__ void __launch_bounds__(1024, 1) select_shared_kernel(const SharedParams P) {
   extern __shared__ __align__(16) unsigned char smem[];
   __shared__ uint64_t stage_bar;
   __shared__ uint32_t s_g;
+#ifdef GPUAR_TIMELINE
+  TL_CTA(0, tl_now());
+  {
+    uint32_t smid;
+    asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+    TL_CTA(3, smid);
+  }
+#endif
   // Programmatic dependent launch: this grid may be resident before the previous kernel of
   // the stream has finished (its CTAs fill the SM slots freed by that kernel's tail).  Before
   // the wait below it touches only what this handle's set_propensities kernels produced --
@@ -450,6 +473,9 @@ __global__ void __launch_bounds__(1024, 1) select_shared_kernel(const SharedPara
   // every prerequisite grid complete; then let the next launch be scheduled early
   pdl_wait();
   pdl_launch_dependents();
+#ifdef GPUAR_TIMELINE
+  TL_CTA(1, tl_now());
+#endif
   // the next launch's ticket set (its previous user, launch n - 1, has completed)
   if (blockIdx.x == 0 && threadIdx.x < kStripes) P.ctr->next[P.phase ^ 1u][threadIdx.x] = 0ull;
 
@@ -476,6 +502,9 @@ __global__ void __launch_bounds__(1024, 1) select_shared_kernel(const SharedPara
   __syncthreads();        // publishes the barrier's initialisation and s_g
   stage_wait(&stage_bar);  // (also before an early exit: no copy may outlive the CTA)
   if (invalid || zero) return;  // uniform over the grid; the tickets are untouched
+#ifdef GPUAR_TIMELINE
+  TL_CTA(2, tl_now());
+#endif
 
   // ---- phase C: trials
   const uint32_t warp_global = tid >> 5;
@@ -515,6 +544,9 @@ __global__ void __launch_bounds__(1024, 1) select_shared_kernel(const SharedPara
     warp_loop<PATH, MULTI>(P, ts, sbase, pl);
   else
     trial_loop<PATH, MULTI>(P, ts, sbase, g, pl);
+#ifdef GPUAR_TIMELINE
+  if ((threadIdx.x & 31u) == 0u) g_tl[P.epoch & 1u][kTlCta + warp_global] = tl_now();
+#endif
 }
 
 template <int PATH>
@@ -524,6 +556,12 @@ void set_limit(int bytes) {
 }
 
 }  // namespace
+
+#ifdef GPUAR_TIMELINE
+extern "C" int gpuar_dbg_timeline(void* host, size_t bytes) {
+  return (int)cudaMemcpyFromSymbol(host, g_tl, bytes < sizeof(g_tl) ? bytes : sizeof(g_tl));
+}
+#endif
 
 cudaError_t launch_select_shared(const SharedParams& p, int path, int grid, int block, cudaStream_t st, bool pdl) {
   const size_t sh = p.smem_bytes;
