@@ -74,6 +74,21 @@ __device__ __forceinline__ Philox4 item_call(const TrialStream& ts, uint32_t c, 
     return ts(c, sel);  // e_lo from the (uniform) stream
 }
 
+#ifdef GPUAR_TIMELINE
+// Diagnostic build only (scripts/diag_timeline.py; never in libgpuar.so): %globaltimer stamps
+// of the last two launches (slot = epoch & 1): per CTA [entry, after the PDL wait, trials
+// start, %smid], per warp its exit and (at kTlCta + 16384 + warp) when its pool ran dry.
+constexpr uint32_t kTlCta = 4u * 1024u, kTlN = kTlCta + 32u * 1024u;
+__device__ unsigned long long g_tl[2][kTlN];
+__device__ __forceinline__ unsigned long long tl_now() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+#define TL_CTA(k, v) \
+  if (threadIdx.x == 0) g_tl[P.epoch & 1u][4u * blockIdx.x + (k)] = (v)
+#endif
+
 // Work distribution: the K selections are cut into kStripes contiguous stripes; warp w
 // belongs to stripe w % kStripes, takes a static first chunk of it, then grabs `grab`
 // selections at a time from the stripe's ticket until the stripe is exhausted.  kStripes
@@ -89,6 +104,9 @@ struct Pool {
   unsigned long long* tickets;   // this launch's ticket set (DevCounters::next[phase])
   uint32_t stripe;
   bool exhausted;
+#ifdef GPUAR_TIMELINE
+  uint32_t tl_slot;
+#endif
 
   // Lane 0 issues the atomic for the chunk after the current one; its latency (~1 us under
   // contention) overlaps the current chunk's work instead of stalling the warp.
@@ -102,6 +120,9 @@ struct Pool {
     const unsigned long long b = __shfl_sync(kFull, pending, 0);
     if (b >= hi) {
       exhausted = true;
+#ifdef GPUAR_TIMELINE
+      if (lane == 0u) g_tl[tl_slot][kTlCta + 16384u + ((blockIdx.x * blockDim.x + threadIdx.x) >> 5)] = tl_now();
+#endif
       return false;
     }
     next = (uint32_t)b;
@@ -404,20 +425,6 @@ __device__ __forceinline__ uint32_t choose_team(float p, uint32_t K, uint32_t nw
 
 constexpr uint32_t kPreTau = 8;  // tau values per thread computed before the PDL wait
 
-#ifdef GPUAR_TIMELINE
-// Diagnostic build only (scripts/diag_timeline.py; never in libgpuar.so): %globaltimer stamps
-// of the last two launches (slot = epoch & 1): per CTA [entry, after the PDL wait, trials
-// start, %smid], per warp its exit.
-constexpr uint32_t kTlCta = 4u * 1024u, kTlN = kTlCta + 32u * 1024u;
-__device__ unsigned long long g_tl[2][kTlN];
-__device__ __forceinline__ unsigned long long tl_now() {
-  unsigned long long t;
-  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-  return t;
-}
-#define TL_CTA(k, v) \
-  if (threadIdx.x == 0) g_tl[P.epoch & 1u][4u * blockIdx.x + (k)] = (v)
-#endif
 
 template <int PATH, bool MULTI>
 __global__ void __launch_bounds__(1024, 1) select_shared_kernel(const SharedParams P) {
@@ -522,6 +529,9 @@ __global__ void __launch_bounds__(1024, 1) select_shared_kernel(const SharedPara
   unsigned long long grab = max(teams, min((unsigned long long)st.grab, max(2ull * teams, fair / 8ull)));
   if (P.grab_override) grab = P.grab_override;
   Pool pl;
+#ifdef GPUAR_TIMELINE
+  pl.tl_slot = P.epoch & 1u;
+#endif
   pool_init(pl, K, nwarps, warp_global, first, grab, P.ctr->next[P.phase], P.no_prefetch == 0u);
   const TrialStream ts(P.seed_lo, P.seed_hi, P.epoch);
   if (g == 1u) {

@@ -90,6 +90,15 @@ def main():
     smin = np.array([we[st == k].min() for k in range(64)])
     print("  stripe last-exit quantiles 0/50/100 %:", " ".join(f"{q:.2f}" for q in np.percentile(smax, [0, 50, 100])),
           "| within-stripe spread mean", f"{(smax - smin).mean():.2f}", "max", f"{(smax - smin).max():.2f}")
+    # when each warp's pool ran dry (0: never asked, e.g. static chunks only) and its tail after
+    dry = cur[kTlCta + 16384:kTlCta + 16384 + ncta * wpc].astype(np.int64)
+    ok = dry > 0
+    if ok.any():
+        ex = c_w.reshape(-1)
+        print("  pool dry (after prev call end) quantiles 0/10/50/90/100 %:",
+              " ".join(f"{q:.2f}" for q in np.percentile((dry[ok] - t0) / 1e3, [0, 10, 50, 90, 100])))
+        print("  warp tail (exit - dry) quantiles 0/10/50/90/100 %:",
+              " ".join(f"{q:.2f}" for q in np.percentile((ex[ok] - dry[ok]) / 1e3, [0, 10, 50, 90, 100])))
     print(f"  team {sel.last_team}")
 
 
