@@ -155,7 +155,12 @@ __device__ __forceinline__ void pool_init(Pool& pl, uint32_t K, uint32_t nwarps,
   // nothing static and no dynamic part left in the stripe: done without touching the ticket
   pl.exhausted = pl.next >= pl.end && pl.dbase >= hi;
   pl.pending = ~0ull;
-  if (ahead && pl.dbase < hi) pl.prefetch(threadIdx.x & 31u);
+}
+
+// The first ticket prefetch (after the PDL wait: the launch's ticket set is only known to be
+// zeroed once the previous launch has completed).
+__device__ __forceinline__ void pool_start(Pool& pl, uint32_t lane) {
+  if (pl.ahead && pl.dbase < pl.hi) pl.prefetch(lane);
 }
 
 // Hand idle teams (leader lanes in `need`) the next selections of the warp's pool.
@@ -331,47 +336,56 @@ __device__ __forceinline__ void lane_loop(const SharedParams& P, const TrialStre
 // Whole-warp teams (g = 32): the warp works its selections one after another, 64 trials
 // per round, like the matrix kernel -- no per-round team bookkeeping, ~15 instructions of
 // overhead per selection (pool refill by lane 0 once per `grab` selections).
+// warp_select: work item `my` by the whole warp; id / tr on every lane.
 template <int PATH, bool MULTI>
-__device__ __forceinline__ void warp_loop(const SharedParams& P, const TrialStream& ts, uint32_t sbase, Pool pl) {
+__device__ __forceinline__ void warp_select(const SharedParams& P, const TrialStream& ts, uint32_t sbase, uint32_t my,
+                                            uint32_t lane, int32_t& id, uint32_t& tr) {
   const uint32_t M = P.M;
   const uint32_t half = P.max_trials >> 1;
   const uint32_t calls = half + (P.max_trials & 1u);
   const uint32_t free_end = half & ~31u;  // rounds starting below it need no cap test
+  uint32_t sel, elo;
+  item_words<MULTI>(P, ts, my, sel, elo);
+  id = -1;
+  tr = P.max_trials;
+  // one round: calls [c0, c0 + 32); CAP: test the trials against max_trials (only rounds
+  // reaching past half = floor(max_trials / 2) need it)
+  auto round = [&](uint32_t c0, auto cap) -> bool {
+    const uint32_t c = c0 + lane;
+    const Philox4 x = item_call<MULTI>(ts, c, sel, elo);
+    const uint32_t j0 = __umulhi(x.x, M);
+    const uint32_t j1 = __umulhi(x.z, M);
+    const bool r0 = accept<PATH>(x.y, j0, sbase, P.thr, P.group_shift);
+    const bool r1 = accept<PATH>(x.w, j1, sbase, P.thr, P.group_shift);
+    const bool a0 = (!decltype(cap)::value || c < calls) & r0;
+    const bool a1 = (!decltype(cap)::value || c < half) & r1;
+    const uint32_t b = __ballot_sync(kFull, a0 || a1);
+    if (b != 0u) {
+      const uint32_t w = __ffs(b) - 1;
+      id = (int32_t)__shfl_sync(kFull, a0 ? j0 : j1, w);
+      tr = __shfl_sync(kFull, a0 ? 2u * c + 1u : 2u * c + 2u, w);
+      return true;
+    }
+    return false;
+  };
+  uint32_t c0 = 0;
+  bool hit = false;
+  for (; c0 < free_end; c0 += 32u)
+    if ((hit = round(c0, std::false_type{}))) break;
+  if (!hit)
+    for (; c0 < calls; c0 += 32u)
+      if (round(c0, std::true_type{})) break;
+}
+
+template <int PATH, bool MULTI>
+__device__ __forceinline__ void warp_loop(const SharedParams& P, const TrialStream& ts, uint32_t sbase, Pool pl) {
   const uint32_t lane = threadIdx.x & 31u;
   while (!pl.exhausted) {
     if (pl.next >= pl.end && !pl.refill(lane)) break;
     const uint32_t my = pl.next++;
-    uint32_t sel, elo;
-    item_words<MULTI>(P, ts, my, sel, elo);
-    int32_t id = -1;
-    uint32_t tr = P.max_trials;
-    // one round: calls [c0, c0 + 32); CAP: test the trials against max_trials (only rounds
-    // reaching past half = floor(max_trials / 2) need it)
-    auto round = [&](uint32_t c0, auto cap) -> bool {
-      const uint32_t c = c0 + lane;
-      const Philox4 x = item_call<MULTI>(ts, c, sel, elo);
-      const uint32_t j0 = __umulhi(x.x, M);
-      const uint32_t j1 = __umulhi(x.z, M);
-      const bool r0 = accept<PATH>(x.y, j0, sbase, P.thr, P.group_shift);
-      const bool r1 = accept<PATH>(x.w, j1, sbase, P.thr, P.group_shift);
-      const bool a0 = (!decltype(cap)::value || c < calls) & r0;
-      const bool a1 = (!decltype(cap)::value || c < half) & r1;
-      const uint32_t b = __ballot_sync(kFull, a0 || a1);
-      if (b != 0u) {
-        const uint32_t w = __ffs(b) - 1;
-        id = (int32_t)__shfl_sync(kFull, a0 ? j0 : j1, w);
-        tr = __shfl_sync(kFull, a0 ? 2u * c + 1u : 2u * c + 2u, w);
-        return true;
-      }
-      return false;
-    };
-    uint32_t c0 = 0;
-    bool hit = false;
-    for (; c0 < free_end; c0 += 32u)
-      if ((hit = round(c0, std::false_type{}))) break;
-    if (!hit)
-      for (; c0 < calls; c0 += 32u)
-        if (round(c0, std::true_type{})) break;
+    int32_t id;
+    uint32_t tr;
+    warp_select<PATH, MULTI>(P, ts, sbase, my, lane, id, tr);
     if (lane == 0u) {
       P.idx[my] = id;
       if (P.trials) P.trials[my] = tr;
@@ -421,6 +435,52 @@ __device__ __forceinline__ uint32_t choose_team(float p, uint32_t K, uint32_t nw
     }
   }
   return best;
+}
+
+// The warp's work-stealing pool: static first chunk of half a warp's fair share, then grabs
+// of ~8192 expected trials (st.grab), at most an eighth of the fair share (but two teams'
+// worth), at least one selection per team; tickets are prefetched one chunk ahead (the first
+// by pool_start, after the PDL wait).  (fair = max(1, K / warps) and the static chunk come
+// from the host, launch_select: two 64-bit divisions per warp were ~100 of the ~170 set-up
+// instructions of every warp.)
+__device__ __forceinline__ void pool_setup(const SharedParams& P, const DevStats& st, uint32_t g, uint32_t nwarps,
+                                           uint32_t warp_global, Pool& pl) {
+  const unsigned long long teams = 32u / g;
+  const unsigned long long fair = P.fair;
+  const unsigned long long first = max(teams, (unsigned long long)P.first_base);
+  // (r01 sweep, GPUAR_GRAB: c2 best at 2 with prefetch; heavy tails (st.grab = 1) at 1)
+  unsigned long long grab = max(teams, min((unsigned long long)st.grab, max(2ull * teams, fair / 8ull)));
+  if (P.grab_override) grab = P.grab_override;
+#ifdef GPUAR_TIMELINE
+  pl.tl_slot = P.epoch & 1u;
+#endif
+  pool_init(pl, P.K, nwarps, warp_global, first, grab, P.ctr->next[P.phase], P.no_prefetch == 0u);
+}
+
+// The trial loop of the CTA's team size g.
+template <int PATH, bool MULTI>
+__device__ __forceinline__ void run_trials(const SharedParams& P, const DevStats& st, const TrialStream& ts,
+                                           uint32_t sbase, uint32_t g, const Pool& pl) {
+  if (g == 1u) {
+    // two calls per round exactly where choose_team priced them (1/128 <= p <= 1/4); a
+    // forced g = 1 (GPUAR_TEAM) outside that range runs the one-call loop
+    const bool two = st.p <= 0.25f && st.p >= 1.0f / 128.0f;
+    if (P.trials) {
+      if (two)
+        lane_loop<PATH, 2, MULTI, true>(P, ts, sbase, pl);
+      else
+        lane_loop<PATH, 1, MULTI, true>(P, ts, sbase, pl);
+    } else {
+      if (two)
+        lane_loop<PATH, 2, MULTI, false>(P, ts, sbase, pl);
+      else
+        lane_loop<PATH, 1, MULTI, false>(P, ts, sbase, pl);
+    }
+  } else if (g == 32u) {
+    warp_loop<PATH, MULTI>(P, ts, sbase, pl);
+  } else {
+    trial_loop<PATH, MULTI>(P, ts, sbase, g, pl);
+  }
 }
 
 constexpr uint32_t kPreTau = 8;  // tau values per thread computed before the PDL wait
@@ -517,45 +577,104 @@ __global__ void __launch_bounds__(1024, 1) select_shared_kernel(const SharedPara
   const uint32_t warp_global = tid >> 5;
   const uint32_t g = s_g;
   if (tid == 0) P.ctr->team = g;
-  // static first chunk: half of a warp's fair share; then grabs of ~8192 expected trials
-  // (st.grab), at most an eighth of the fair share (but two teams' worth), at least one
-  // selection per team; tickets are prefetched one chunk ahead.
-  // (fair = max(1, K / warps) and the static chunk come from the host, launch_select: two
-  // 64-bit divisions per warp were ~100 of the ~170 set-up instructions of every warp)
-  const unsigned long long teams = 32u / g;
-  const unsigned long long fair = P.fair;
-  const unsigned long long first = max(teams, (unsigned long long)P.first_base);
-  // (r01 sweep, GPUAR_GRAB: c2 best at 2 with prefetch; heavy tails (st.grab = 1) at 1)
-  unsigned long long grab = max(teams, min((unsigned long long)st.grab, max(2ull * teams, fair / 8ull)));
-  if (P.grab_override) grab = P.grab_override;
   Pool pl;
-#ifdef GPUAR_TIMELINE
-  pl.tl_slot = P.epoch & 1u;
-#endif
-  pool_init(pl, K, nwarps, warp_global, first, grab, P.ctr->next[P.phase], P.no_prefetch == 0u);
+  pool_setup(P, st, g, nwarps, warp_global, pl);
+  pool_start(pl, threadIdx.x & 31u);
   const TrialStream ts(P.seed_lo, P.seed_hi, P.epoch);
-  if (g == 1u) {
-    // two calls per round exactly where choose_team priced them (1/128 <= p <= 1/4); a
-    // forced g = 1 (GPUAR_TEAM) outside that range runs the one-call loop
-    const bool two = st.p <= 0.25f && st.p >= 1.0f / 128.0f;
-    if (P.trials) {
-      if (two)
-        lane_loop<PATH, 2, MULTI, true>(P, ts, sbase, pl);
-      else
-        lane_loop<PATH, 1, MULTI, true>(P, ts, sbase, pl);
-    } else {
-      if (two)
-        lane_loop<PATH, 2, MULTI, false>(P, ts, sbase, pl);
-      else
-        lane_loop<PATH, 1, MULTI, false>(P, ts, sbase, pl);
-    }
-  }
-  else if (g == 32u)
-    warp_loop<PATH, MULTI>(P, ts, sbase, pl);
-  else
-    trial_loop<PATH, MULTI>(P, ts, sbase, g, pl);
+  run_trials<PATH, MULTI>(P, st, ts, sbase, g, pl);
 #ifdef GPUAR_TIMELINE
   if ((threadIdx.x & 31u) == 0u) g_tl[P.epoch & 1u][kTlCta + warp_global] = tl_now();
+#endif
+}
+
+// Fewer work items than threads (c1, c2): at most one tau per thread, so there is no tau to
+// compute before the PDL wait (it gained nothing there); instead whole-warp
+// teams (g = 32) work the first <= 32 items of their static chunk before the wait -- pure
+// arithmetic on the staged thresholds and the statistics, lane k holding item k's result
+// until the stores after the wait.  On an SM the previous call left early this overlaps that
+// call's end, which otherwise idles ~2.7 us of a 28 us c2 call (scripts/diag_timeline.py).
+// The same outputs as select_shared_kernel; a separate kernel so that the K >= threads
+// configurations keep their code (the pre-wait loop costs registers: 46 -> ~60).
+template <int PATH>
+__global__ void __launch_bounds__(1024, 1) select_shared_pre_kernel(const SharedParams P) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  __shared__ uint64_t stage_bar;
+  __shared__ uint32_t s_g;
+#ifdef GPUAR_TIMELINE
+  TL_CTA(0, tl_now());
+  {
+    uint32_t smid;
+    asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+    TL_CTA(3, smid);
+  }
+#endif
+  // before the wait: only the thresholds / prefilter and the statistics (see select_shared_kernel)
+  const uint32_t sbase = (PATH == kPathSmemF32) ? stage_issue(smem, P.thr, 4u * P.M, &stage_bar)
+                                                : stage_issue(smem, P.prefilter, 2u * P.n_pref, &stage_bar);
+  const DevStats st = *P.stats;
+  const uint32_t tid = blockIdx.x * blockDim.x + threadIdx.x;
+  const uint32_t nthreads = gridDim.x * blockDim.x;
+  const bool invalid = st.valid == 0u;
+  const bool zero = st.amax_bits == 0u;
+  const uint32_t K = P.K;
+  const uint32_t nwarps = nthreads >> 5;
+  if (threadIdx.x == 0) s_g = P.team_override ? P.team_override : choose_team(st.p, K, nwarps);  // once per CTA
+  __syncthreads();         // publishes the barrier's initialisation and s_g
+  stage_wait(&stage_bar);  // (also before an early exit: no copy may outlive the CTA)
+  const uint32_t lane = threadIdx.x & 31u;
+  const uint32_t warp_global = tid >> 5;
+  const uint32_t g = s_g;
+  Pool pl;
+  pool_setup(P, st, g, nwarps, warp_global, pl);
+  const TrialStream ts(P.seed_lo, P.seed_hi, P.epoch);
+  uint32_t pre_n = 0;
+  const uint32_t pre_base = pl.next;
+  int32_t pre_id = -1;
+  uint32_t pre_tr = 0;
+  if (g == 32u && !invalid && !zero) {
+    pre_n = min(32u, pl.end - pl.next);
+    for (uint32_t k = 0; k < pre_n; ++k) {
+      int32_t id;
+      uint32_t tr;
+      warp_select<PATH, false>(P, ts, sbase, pre_base + k, lane, id, tr);
+      if (lane == k) {
+        pre_id = id;
+        pre_tr = tr;
+      }
+    }
+    pl.next += pre_n;
+  }
+  // every prerequisite grid complete; then let the next launch be scheduled early
+  pdl_wait();
+  pdl_launch_dependents();
+#ifdef GPUAR_TIMELINE
+  TL_CTA(1, tl_now());
+#endif
+  // the next launch's ticket set (its previous user, launch n - 1, has completed)
+  if (blockIdx.x == 0 && threadIdx.x < kStripes) P.ctr->next[P.phase ^ 1u][threadIdx.x] = 0ull;
+  // tau (at most one per thread); degenerate / invalid outputs
+  for (uint32_t s = tid; s < K; s += nthreads) {
+    if (invalid || zero) {
+      P.idx[s] = -1;
+      if (P.trials) P.trials[s] = 0u;
+      if (P.tau) P.tau[s] = invalid ? __uint_as_float(0x7fc00000u) : __uint_as_float(kInfBits);
+    } else if (P.tau) {
+      P.tau[s] = __fdiv_rn(neg_log_u1(P.seed_lo, P.seed_hi, P.s0 + s, P.epoch), st.a0f);
+    }
+  }
+  if (invalid || zero) return;  // uniform over the grid; the tickets are untouched
+#ifdef GPUAR_TIMELINE
+  TL_CTA(2, tl_now());
+#endif
+  if (lane < pre_n) {
+    P.idx[pre_base + lane] = pre_id;
+    if (P.trials) P.trials[pre_base + lane] = pre_tr;
+  }
+  if (tid == 0) P.ctr->team = g;
+  pool_start(pl, lane);
+  run_trials<PATH, false>(P, st, ts, sbase, g, pl);
+#ifdef GPUAR_TIMELINE
+  if (lane == 0u) g_tl[P.epoch & 1u][kTlCta + warp_global] = tl_now();
 #endif
 }
 
@@ -563,6 +682,7 @@ template <int PATH>
 void set_limit(int bytes) {
   set_max_dynamic_smem(select_shared_kernel<PATH, false>, bytes);
   set_max_dynamic_smem(select_shared_kernel<PATH, true>, bytes);
+  set_max_dynamic_smem(select_shared_pre_kernel<PATH>, bytes);
 }
 
 }  // namespace
@@ -576,15 +696,20 @@ extern "C" int gpuar_dbg_timeline(void* host, size_t bytes) {
 cudaError_t launch_select_shared(const SharedParams& p, int path, int grid, int block, cudaStream_t st, bool pdl) {
   const size_t sh = p.smem_bytes;
   const bool multi = p.n_epochs > 1u;
+  // fewer work items than threads: the variant that works trials before the PDL wait
+  const bool pre = !multi && (uint64_t)p.K < (uint64_t)grid * (uint64_t)block;
   switch (path) {
     case kPathSmemF32:
       return multi ? launch_pdl(select_shared_kernel<kPathSmemF32, true>, grid, block, sh, st, pdl, p)
+             : pre ? launch_pdl(select_shared_pre_kernel<kPathSmemF32>, grid, block, sh, st, pdl, p)
                    : launch_pdl(select_shared_kernel<kPathSmemF32, false>, grid, block, sh, st, pdl, p);
     case kPathSmemBf16:
       return multi ? launch_pdl(select_shared_kernel<kPathSmemBf16, true>, grid, block, sh, st, pdl, p)
+             : pre ? launch_pdl(select_shared_pre_kernel<kPathSmemBf16>, grid, block, sh, st, pdl, p)
                    : launch_pdl(select_shared_kernel<kPathSmemBf16, false>, grid, block, sh, st, pdl, p);
     case kPathSmemGroup:
       return multi ? launch_pdl(select_shared_kernel<kPathSmemGroup, true>, grid, block, sh, st, pdl, p)
+             : pre ? launch_pdl(select_shared_pre_kernel<kPathSmemGroup>, grid, block, sh, st, pdl, p)
                    : launch_pdl(select_shared_kernel<kPathSmemGroup, false>, grid, block, sh, st, pdl, p);
     default:
       return cudaErrorInvalidValue;

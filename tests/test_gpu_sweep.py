@@ -316,3 +316,26 @@ def test_reregistered_vectors_back_to_back():
         ref = oracle.ar_select(vecs[v], K, seed=SEED, epoch=e, nthreads=8)
         np.testing.assert_array_equal(o[0].cpu().numpy(), ref["idx"])
         np.testing.assert_array_equal(o[2].cpu().numpy().view(np.uint32), ref["trials"])
+
+
+# ---------------------------------------------------------------- the pre-wait kernel boundary
+
+@pytest.mark.parametrize("delta", [-1, 0])
+def test_pre_wait_kernel_boundary(delta):
+    """Fewer work items than resident threads launch select_shared_pre_kernel (whole-warp
+    teams work their static chunk before the PDL wait, results held in registers until the
+    stores after it); K = threads launches select_shared_kernel.  Both sides of the switch,
+    back to back (PDL overlap of consecutive launches, alternating ticket sets), bit-exact."""
+    from paper_1404_0027_b200 import Selector
+    threads = torch.cuda.get_device_properties(0).multi_processor_count * 1024
+    K = threads + delta
+    a = np.ascontiguousarray(synth.yeast_like(), np.float32)
+    sel = Selector(a.size, K, SEED)
+    sel.set_selection_offset(77)
+    sel.epoch = 5
+    sel.set_propensities(torch.from_numpy(a).cuda())
+    outs = [sel.select(K) for _ in range(3)]
+    sel.sync()
+    assert sel.last_team == 32
+    for i, out in enumerate(outs):
+        _check(out, oracle.ar_select(a, K, seed=SEED, epoch=5 + i, s0=77, nthreads=16))
