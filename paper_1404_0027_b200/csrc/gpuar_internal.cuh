@@ -372,6 +372,73 @@ __device__ __forceinline__ void row_reduce(uint32_t row_s, uint32_t M, uint32_t 
   acc_out = acc;
 }
 
+// The same reduction, bit for bit (same chunks, same pairwise sums, same binary64 order), with
+// counted loops over a running shared address: per row the loop control is a compare and an
+// add per two 512-chunks instead of the ~30 instructions of the generic `b0 + 512 <= M` loop
+// the compiler unrolls by two.  Used where the trials are ALU-heavy (the SSA kernel: s1 +3.2 %;
+// the argmin rule on rows: +1.3 %, A/B on one box); the classic matrix kernel keeps
+// row_reduce, under which its burst read rate measured 1 % higher (sustained 2 % lower).
+__device__ __forceinline__ void row_reduce_counted(uint32_t row_s, uint32_t M, uint32_t lane, uint32_t& mx_out,
+                                                   double& acc_out) {
+  uint32_t mx = 0;
+  double acc = 0.0;
+  uint32_t p = row_s + 4u * lane;
+  const uint32_t n512 = M >> 9;
+  // one 512-chunk: 16 conflict-free loads per lane, pairwise binary32 sum of them (FADD2)
+  auto chunk = [&](uint32_t q) -> float {
+    float v[16];
+#pragma unroll
+    for (int k = 0; k < 16; ++k) {
+      v[k] = lds_f32(q + 128u * k);
+      mx = max(mx, __float_as_uint(v[k]));
+    }
+    float2 w[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) w[k] = make_float2(v[2 * k], v[2 * k + 1]);
+    const float2 rr = fadd2_rn(fadd2_rn(fadd2_rn(w[0], w[1]), fadd2_rn(w[2], w[3])),
+                               fadd2_rn(fadd2_rn(w[4], w[5]), fadd2_rn(w[6], w[7])));
+    return __fadd_rn(rr.x, rr.y);
+  };
+  uint32_t i = 0;
+#pragma unroll 1
+  for (; i + 2u <= n512; i += 2u, p += 4096u) {  // two chunks per step: 32 loads in flight
+    const float s0 = chunk(p), s1 = chunk(p + 2048u);
+    acc += (double)s0;
+    acc += (double)s1;
+  }
+  if (i < n512) {
+    acc += (double)chunk(p);
+    p += 2048u;
+  }
+  if (M & 256u) {
+    float v[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      v[k] = lds_f32(p + 128u * k);
+      mx = max(mx, __float_as_uint(v[k]));
+    }
+    const float2 rr = fadd2_rn(fadd2_rn(make_float2(v[0], v[1]), make_float2(v[2], v[3])),
+                               fadd2_rn(make_float2(v[4], v[5]), make_float2(v[6], v[7])));
+    acc += (double)__fadd_rn(rr.x, rr.y);
+    p += 1024u;
+  }
+  const uint32_t b0 = M & ~255u;
+  if (b0 < M) {  // tail: warp-uniform trip count, one predicated load per lane per step
+    float sum = 0.f;
+#pragma unroll 1
+    for (uint32_t j = b0 + lane; j < M + lane; j += 32u, p += 128u) {
+      const float v = (j < M) ? lds_f32(p) : 0.f;
+      mx = max(mx, __float_as_uint(v));
+      sum = __fadd_rn(sum, v);  // + 0.0 leaves a sum of non-negative values unchanged
+    }
+    acc += (double)sum;
+  }
+  mx_out = __reduce_max_sync(kFull, mx);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(kFull, acc, o);
+  acc_out = acc;
+}
+
 // Programmatic dependent launch (PDL, sm_90+): griddepcontrol.wait blocks until every
 // prerequisite grid of the stream has completed and its memory is visible; launch_dependents
 // lets the next PDL-launched grid be scheduled before this one finishes.

@@ -455,7 +455,10 @@ __global__ void __launch_bounds__(MAXW * 32, 1) select_rows_kernel(const RowsPar
     // ---- alpha_max (max of bit patterns) and alpha_0 in the fixed order of row_reduce
     uint32_t mx;
     double acc;
-    row_reduce(row_s, M, lane, mx, acc);
+    if constexpr (MODE == kRuleArgmin)
+      row_reduce_counted(row_s, M, lane, mx, acc);
+    else
+      row_reduce(row_s, M, lane, mx, acc);
 
     if constexpr (MODE == kModeStats) {
       if (lane == nl32) {

@@ -127,7 +127,7 @@ __global__ void __launch_bounds__(768, 1) ssa_kernel(const SsaParams P) {
       }
       uint32_t mx;
       double acc;
-      row_reduce(row_s, M, lane, mx, acc);
+      row_reduce_counted(row_s, M, lane, mx, acc);
       __syncwarp();  // row complete before the gathers
       if (mx >= kInfBits) {  // invalid propensity: sticky EPROPENSITY, stop this realization
         if (lane == 0) atomicOr(&P.ctr->err, 1u);
