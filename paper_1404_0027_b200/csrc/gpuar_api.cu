@@ -61,6 +61,7 @@ struct gpuar_handle {
   uint32_t team_override = 0;
   bool pdl = true;            // programmatic dependent launch of the shared-vector kernels
   uint32_t no_prefetch = 0;
+  uint32_t no_endgame = 0;
   double* d_part_sum = nullptr;
   uint32_t* d_part_max = nullptr;
   int stats_blocks = 1;
@@ -233,6 +234,7 @@ int launch_select(gpuar_handle* h, const float* alpha, int64_t rows, int64_t ld,
     p.grab_override = h->grab_override;
     p.team_override = h->team_override;
     p.no_prefetch = h->no_prefetch;
+    p.no_endgame = h->no_endgame;
     if (h->rule == kRuleArgmin) {
       e = launch_argmin_shared(p, h->am_smem, h->am_grid, 256, st, h->pdl);
     } else if (h->rule == kRuleIT) {
@@ -371,6 +373,7 @@ int gpuar_create(gpuar_t* out, int64_t M, int64_t K, uint64_t seed) {
     h->team_override = (g >= 1 && g <= 32 && (g & (g - 1)) == 0) ? (uint32_t)g : 0u;
   }
   h->no_prefetch = (uint32_t)std::max(0, env_int("GPUAR_NO_PREFETCH", 0));
+  h->no_endgame = (uint32_t)std::max(0, env_int("GPUAR_NO_ENDGAME", 0));
   h->pdl = env_int("GPUAR_NO_PDL", 0) == 0;
   cudaError_t e = cudaMalloc(&h->d_stats, sizeof(DevStats));
   if (e == cudaSuccess) e = cudaMalloc(&h->d_ctr, sizeof(DevCounters));

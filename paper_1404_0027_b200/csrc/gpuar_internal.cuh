@@ -74,6 +74,7 @@ struct SharedParams {
                              // fair <= 4, ceil(ceil(K / kStripes) / max(1, warps / kStripes))
                              // (static chunks that cover each stripe: no tickets at all)
   uint32_t no_prefetch;      // tuning: 1 = fetch tickets on demand
+  uint32_t no_endgame;       // tuning: 1 = the lane loop never hands its last selections to the whole warp
   uint32_t phase;            // ticket set of this launch (DevCounters::next)
   // multi-epoch launches (gpuar_select_epochs): K above is the number of work items
   // n_epochs * Ksel; item q is selection q mod Ksel at epoch + q / Ksel, output slot q

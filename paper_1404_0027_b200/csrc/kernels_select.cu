@@ -254,6 +254,54 @@ __device__ __forceinline__ void trial_loop(const SharedParams& P, const TrialStr
   }
 }
 
+// The endgame of the lane loop: the warp's pool is empty and few lanes still hold a selection
+// (each at its own next call c).  Every lane then works one of them at a time, rounds of calls
+// [c0, c0 + 32) from c0 = c: the lowest accepting lane (even trial first) is the first accept at
+// or after call c, so the result is the one the lane itself would have reached (R6),
+// in ~1 / (1 - (1 - p)^64) warp rounds instead of the geometric tail of the slowest lane.
+template <int PATH, bool MULTI>
+__device__ __forceinline__ void warp_rounds(const SharedParams& P, const TrialStream& ts, uint32_t sbase,
+                                            uint32_t sel, uint32_t elo, uint32_t c0, uint32_t lane, int32_t& id,
+                                            uint32_t& tr) {
+  const uint32_t M = P.M;
+  const uint32_t half = P.max_trials >> 1;
+  const uint32_t calls = half + (P.max_trials & 1u);
+  id = -1;
+  tr = P.max_trials;
+#pragma unroll 1
+  for (; c0 < calls; c0 += 32u) {
+    const uint32_t c = c0 + lane;
+    const Philox4 x = item_call<MULTI>(ts, c, sel, elo);
+    const uint32_t j0 = __umulhi(x.x, M);
+    const uint32_t j1 = __umulhi(x.z, M);
+    const bool a0 = (c < calls) & accept<PATH>(x.y, j0, sbase, P.thr, P.group_shift);
+    const bool a1 = (c < half) & accept<PATH>(x.w, j1, sbase, P.thr, P.group_shift);
+    const uint32_t b = __ballot_sync(kFull, a0 || a1);
+    if (b != 0u) {
+      const uint32_t w = __ffs(b) - 1;
+      id = (int32_t)__shfl_sync(kFull, a0 ? j0 : j1, w);
+      tr = __shfl_sync(kFull, a0 ? 2u * c + 1u : 2u * c + 2u, w);
+      return;
+    }
+  }
+}
+
+// Largest number of still-busy lanes k for which the endgame above issues fewer warp
+// instructions than letting the lane loop run on: k selections x 1 / (1 - (1 - p)^64) warp
+// rounds of ~77 instructions against the expected maximum of k geometric lane-round counts
+// (H_k / -ln(1 - q) + 1/2, q = 1 - (1 - p)^(2 nc), H_k ~ ln k + 0.5772 + 1 / 2k) of ~117
+// (nc = 1) / ~162 (nc = 2) instructions (the SASS counts of choose_team).  Lane l tests
+// k = l + 1 (the warp cost is linear in k, the lane-loop cost concave: the test holds for
+// k <= T); evaluated by a warp once, when its pool first runs dry.
+__device__ __forceinline__ uint32_t endgame_lanes(float p, uint32_t nc, uint32_t lane) {
+  const float l1 = __logf(fmaxf(1.0f - p, 1e-30f));
+  const float rw = 1.0f / fmaxf(1.0f - __expf(64.0f * l1), 1e-30f);
+  const float L = fmaxf(-2.0f * (float)nc * l1, 1e-30f);
+  const float k = (float)(lane + 1u);
+  const float H = __logf(k) + 0.5772157f + 0.5f / k;
+  return __popc(__ballot_sync(kFull, k * rw * 77.0f < (H / L + 0.5f) * (nc == 2u ? 162.0f : 117.0f)));
+}
+
 // One lane per selection (g = 1, high p): every round each lane makes NC Philox calls (1, or
 // 2 for p <= 1/4) for its own selection; a lane that finishes stores its result and takes the next selection of
 // the warp's pool (one ballot + popc), with no cross-lane data exchange.  At high p most
@@ -261,7 +309,8 @@ __device__ __forceinline__ void trial_loop(const SharedParams& P, const TrialStr
 // idle lane -> one popc and a 32-bit add (selection indices are < K < 2^32); only a chunk
 // boundary takes the general loop (refill / prefetch).
 template <int PATH, int NC, bool MULTI, bool WANT_TR>
-__device__ __forceinline__ void lane_loop(const SharedParams& P, const TrialStream& ts, uint32_t sbase, Pool pl) {
+__device__ __forceinline__ void lane_loop(const SharedParams& P, const TrialStream& ts, uint32_t sbase, Pool pl,
+                                          float p_acc) {
   const uint32_t M = P.M;
   const uint32_t half = P.max_trials >> 1;
   const uint32_t calls = half + (P.max_trials & 1u);
@@ -272,6 +321,7 @@ __device__ __forceinline__ void lane_loop(const SharedParams& P, const TrialStre
   uint32_t my = kNone, sel = 0, elo = 0, c = 0;
   bool active = false;
   uint32_t need = kFull;  // lanes without a selection
+  uint32_t endgame = kNone;  // endgame_lanes, once the pool has run dry
   while (true) {
     if (need != 0u) {  // warp-uniform: hand out selections
       const uint32_t n = __popc(need);
@@ -299,7 +349,30 @@ __device__ __forceinline__ void lane_loop(const SharedParams& P, const TrialStre
           pl.next += min((uint32_t)__popc(need), avail);
           need &= ~__ballot_sync(kFull, mine);
         }
-        if (pl.exhausted && !__any_sync(kFull, active)) break;
+        if constexpr (NC == 1) {
+          if (pl.exhausted && !__any_sync(kFull, active)) break;
+        } else if (pl.exhausted) {
+          // (the two-call loop only: at p > 1/4 the warp takes over at most two lanes and the
+          // extra code cost the one-call loop 5 % on c3 uniform)
+          const uint32_t busy = __ballot_sync(kFull, active);
+          if (busy == 0u) break;
+          if (endgame == kNone) endgame = P.no_endgame ? 0u : endgame_lanes(p_acc, (uint32_t)NC, lane);
+          if ((uint32_t)__popc(busy) <= endgame) {  // the warp finishes the rest one by one
+            for (uint32_t b = busy; b != 0u; b &= b - 1u) {
+              const uint32_t src = __ffs(b) - 1;
+              const uint32_t m = __shfl_sync(kFull, my, src);
+              int32_t id;
+              uint32_t tr;
+              warp_rounds<PATH, MULTI>(P, ts, sbase, __shfl_sync(kFull, sel, src), __shfl_sync(kFull, elo, src),
+                                       __shfl_sync(kFull, c, src), lane, id, tr);
+              if (lane == 0u) {
+                idx_out[m] = id;
+                if constexpr (WANT_TR) tr_out[m] = tr;
+              }
+            }
+            break;
+          }
+        }
       }
     }
     // NC = 1: call c (trials 2c, 2c+1); NC = 2: calls c and c+1 (trials 2c .. 2c+3), decided
@@ -397,7 +470,7 @@ __device__ __forceinline__ void warp_loop(const SharedParams& P, const TrialStre
 // selection (E = 1/p expected trials; SASS counts of the r01 build):
 //   g = 32 (warp_loop): (E/64 + 1/2) rounds x 62 + 15 per selection;
 //   g = 1 (lane_loop): (E + 1)/64 warp-rounds x (72 + 45 P(any lane of the warp finished)),
-//     or with two calls per round (1/128 <= p <= 1/4) (E + 2)/128 warp-rounds x (117 + 45 P(any));
+//     or with two calls per round (1/320 <= p <= 1/4) (E + 2)/128 warp-rounds x (117 + 45 P(any));
 //   1 < g < 32 (trial_loop): (E + g)/64 warp-rounds x (67 + 45 P(any lane finished));
 // (finish costs recalibrated in session 2: ncu counts ~125 warp instructions per lane-loop
 // round when a lane finishes almost every round (c3 exponential, M = 10^4), and the
@@ -405,6 +478,11 @@ __device__ __forceinline__ void warp_loop(const SharedParams& P, const TrialStre
 // times (1 + drain tail), tail = 0.1 T ln(T+1) * warps / K with T = 32/g teams per warp.
 // (The 0.1 is the session-2 team sweep, GPUAR_TEAM: at K = 10^4 the unscaled tail chose
 // g = 32 where g = 4 runs 5 % faster; at K >= 2^16 the tail is too small to move a choice.)
+#ifndef GPUAR_TWO_CALL_MIN_P
+#define GPUAR_TWO_CALL_MIN_P (1.0f / 320.0f)
+#endif
+constexpr float kTwoCallMinP = GPUAR_TWO_CALL_MIN_P;  // the two-call lane loop's lower bound on p
+
 __device__ __forceinline__ uint32_t choose_team(float p, uint32_t K, uint32_t nwarps) {
   const float wk = (float)nwarps / (float)max(K, 1u);
   const float E = 1.0f / fmaxf(p, 1e-30f);
@@ -413,15 +491,17 @@ __device__ __forceinline__ uint32_t choose_team(float p, uint32_t K, uint32_t nw
   float best_cost = (E / 64.0f + 0.5f) * 62.0f + 15.0f;
   best_cost *= 1.0f + 0.06931f * wk;
   // lane loop with two calls per round (p <= 1/4): 128 trials per warp-round at ~117
-  // instructions plus the finish handling.  Considered only up to E = 128: measured +16-20 %
-  // at E = 14 and 73 (c3 exponential M = 10^5, Pareto M = 10^3) but -29 % at E = 292 and
-  // -31 % at E ~ 10^5 (c3 Pareto M = 10^4, c5), where the last selection of each lane
-  // leaves most of the warp idle (the drain term above underrates that tail)
+  // instructions plus the finish handling.  Considered only up to E = 320: before the lane
+  // loop's endgame (the warp takes over its last selections, warp_rounds) it measured +16-20 %
+  // at E = 14 and 73 but -29 % at E = 292 and -31 % at E ~ 10^5, where the last selection of
+  // each lane left most of the warp idle; with the endgame (A/B on one box) +20 % at E = 73
+  // (c3 Pareto M = 10^3), +8 % at E = 188 (M = 10^4), +4 % at E = 266, -2 % at E = 391,
+  // -10 % at E = 1561 and -6 % at E ~ 10^5 (c5): whole-warp teams beyond E = 320
   const float any2 = 1.0f - __expf(128.0f * __logf(fmaxf(1.0f - p, 1e-30f)));
   for (uint32_t g = 1u; g < 32u; g <<= 1) {
     const float T = (float)(32u / g);
     float rounds, round;
-    if (g == 1u && p <= 0.25f && p >= 1.0f / 128.0f) {
+    if (g == 1u && p <= 0.25f && p >= kTwoCallMinP) {
       rounds = (E + 2.0f) / 128.0f;
       round = 117.0f + 45.0f * any2;
     } else {
@@ -464,17 +544,17 @@ __device__ __forceinline__ void run_trials(const SharedParams& P, const DevStats
   if (g == 1u) {
     // two calls per round exactly where choose_team priced them (1/128 <= p <= 1/4); a
     // forced g = 1 (GPUAR_TEAM) outside that range runs the one-call loop
-    const bool two = st.p <= 0.25f && st.p >= 1.0f / 128.0f;
+    const bool two = st.p <= 0.25f && st.p >= kTwoCallMinP;
     if (P.trials) {
       if (two)
-        lane_loop<PATH, 2, MULTI, true>(P, ts, sbase, pl);
+        lane_loop<PATH, 2, MULTI, true>(P, ts, sbase, pl, st.p);
       else
-        lane_loop<PATH, 1, MULTI, true>(P, ts, sbase, pl);
+        lane_loop<PATH, 1, MULTI, true>(P, ts, sbase, pl, st.p);
     } else {
       if (two)
-        lane_loop<PATH, 2, MULTI, false>(P, ts, sbase, pl);
+        lane_loop<PATH, 2, MULTI, false>(P, ts, sbase, pl, st.p);
       else
-        lane_loop<PATH, 1, MULTI, false>(P, ts, sbase, pl);
+        lane_loop<PATH, 1, MULTI, false>(P, ts, sbase, pl, st.p);
     }
   } else if (g == 32u) {
     warp_loop<PATH, MULTI>(P, ts, sbase, pl);

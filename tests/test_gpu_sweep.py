@@ -339,3 +339,28 @@ def test_pre_wait_kernel_boundary(delta):
     assert sel.last_team == 32
     for i, out in enumerate(outs):
         _check(out, oracle.ar_select(a, K, seed=SEED, epoch=5 + i, s0=77, nthreads=16))
+
+
+# ---------------------------------------------------------------- the lane loop's endgame
+
+@pytest.mark.parametrize("M", [1000, 10_000])
+@pytest.mark.parametrize("endgame", [True, False])
+def test_lane_loop_endgame(monkeypatch, M, endgame):
+    """Two-call lane loop (Pareto tails, E ~ 73 / 188) with more items than threads: when a
+    warp's pool runs dry and at most endgame_lanes() lanes still hold a selection, the whole
+    warp finishes them one by one from each lane's own next call (warp_rounds).  Bit-exact
+    against the oracle with the endgame and without it (GPUAR_NO_ENDGAME=1)."""
+    from paper_1404_0027_b200 import Selector
+    monkeypatch.setenv("GPUAR_TEAM", "1")  # (at this K the model picks g = 32 for M = 10^4)
+    if not endgame:
+        monkeypatch.setenv("GPUAR_NO_ENDGAME", "1")
+    K = 300_007
+    a = np.ascontiguousarray(synth.pareto(M), np.float32)
+    sel = Selector(M, K, SEED)
+    sel.set_selection_offset(12345)
+    sel.epoch = 3
+    sel.set_propensities(torch.from_numpy(a).cuda())
+    out = sel.select(K)
+    sel.sync()
+    assert sel.last_team == 1
+    _check(out, oracle.ar_select(a, K, seed=SEED, epoch=3, s0=12345, nthreads=16))
