@@ -66,6 +66,21 @@ __device__ __forceinline__ void item_words(const SharedParams& P, const TrialStr
   }
 }
 
+// -ln(u1) of work item q's tau (R10) from the trial stream's keys
+template <bool MULTI>
+__device__ __forceinline__ float item_neg_log_u1(const SharedParams& P, const TrialStream& ts, uint32_t q) {
+  uint32_t sel, elo;
+  if constexpr (MULTI) {
+    uint32_t e, sl;
+    split_item(q, P.Ksel, P.kinv, e, sl);
+    ts.words(P.epoch + e, P.s0 + sl, sel, elo);
+  } else {
+    sel = ts.sel_word(P.s0 + q);
+    elo = ts.e_lo;
+  }
+  return neg_log_u1_ts(ts, sel, elo);
+}
+
 template <bool MULTI>
 __device__ __forceinline__ Philox4 item_call(const TrialStream& ts, uint32_t c, uint32_t sel, uint32_t elo) {
   if constexpr (MULTI)
@@ -599,6 +614,7 @@ __global__ void __launch_bounds__(1024, 1) select_shared_kernel(const SharedPara
   const bool zero = st.amax_bits == 0u;
   const uint32_t K = P.K;
   const uint32_t nwarps = nthreads >> 5;
+  const TrialStream ts(P.seed_lo, P.seed_hi, P.epoch);  // (also tau's round keys)
   if (threadIdx.x == 0) s_g = P.team_override ? P.team_override : choose_team(st.p, K, nwarps);  // once per CTA
   // tau of this thread's first kPreTau selections, computed before the wait (pure arithmetic
   // on the statistics) and stored after it: on an SM the previous call left early this work
@@ -611,11 +627,7 @@ __global__ void __launch_bounds__(1024, 1) select_shared_kernel(const SharedPara
   for (uint32_t i = 0; i < kPreTau; ++i) {
     const uint32_t s = tid + i * nthreads;
     pre_tau[i] = 0.f;
-    if (want_tau && s < K) {
-      uint32_t e = 0, sl = s;
-      if constexpr (MULTI) split_item(s, P.Ksel, P.kinv, e, sl);
-      pre_tau[i] = __fdiv_rn(neg_log_u1(P.seed_lo, P.seed_hi, P.s0 + sl, P.epoch + e), st.a0f);
-    }
+    if (want_tau && s < K) pre_tau[i] = __fdiv_rn(item_neg_log_u1<MULTI>(P, ts, s), st.a0f);
   }
   // every prerequisite grid complete; then let the next launch be scheduled early
   pdl_wait();
@@ -641,9 +653,7 @@ __global__ void __launch_bounds__(1024, 1) select_shared_kernel(const SharedPara
       if (P.trials) P.trials[s] = 0u;
       if (P.tau) P.tau[s] = invalid ? __uint_as_float(0x7fc00000u) : __uint_as_float(kInfBits);
     } else if (P.tau) {
-      uint32_t e = 0, sl = s;
-      if constexpr (MULTI) split_item(s, P.Ksel, P.kinv, e, sl);
-      P.tau[s] = __fdiv_rn(neg_log_u1(P.seed_lo, P.seed_hi, P.s0 + sl, P.epoch + e), st.a0f);
+      P.tau[s] = __fdiv_rn(item_neg_log_u1<MULTI>(P, ts, s), st.a0f);
     }
   }
   __syncthreads();        // publishes the barrier's initialisation and s_g
@@ -660,7 +670,6 @@ __global__ void __launch_bounds__(1024, 1) select_shared_kernel(const SharedPara
   Pool pl;
   pool_setup(P, st, g, nwarps, warp_global, pl);
   pool_start(pl, threadIdx.x & 31u);
-  const TrialStream ts(P.seed_lo, P.seed_hi, P.epoch);
   run_trials<PATH, MULTI>(P, st, ts, sbase, g, pl);
 #ifdef GPUAR_TIMELINE
   if ((threadIdx.x & 31u) == 0u) g_tl[P.epoch & 1u][kTlCta + warp_global] = tl_now();
@@ -739,7 +748,7 @@ __global__ void __launch_bounds__(1024, 1) select_shared_pre_kernel(const Shared
       if (P.trials) P.trials[s] = 0u;
       if (P.tau) P.tau[s] = invalid ? __uint_as_float(0x7fc00000u) : __uint_as_float(kInfBits);
     } else if (P.tau) {
-      P.tau[s] = __fdiv_rn(neg_log_u1(P.seed_lo, P.seed_hi, P.s0 + s, P.epoch), st.a0f);
+      P.tau[s] = __fdiv_rn(item_neg_log_u1<false>(P, ts, s), st.a0f);
     }
   }
   if (invalid || zero) return;  // uniform over the grid; the tickets are untouched

@@ -98,6 +98,15 @@ struct TrialStream {
     return Philox4{c0, c1, c2, c3};
   }
 
+  // call() with another stream tag: k1t = seed_hi ^ tag
+  __device__ __forceinline__ Philox4 call_tag(uint32_t c, uint32_t sel, uint32_t elo, uint32_t k1t) const {
+    const uint64_t p0 = (uint64_t)kPhiloxM0 * c;
+    uint32_t c0 = sel, c1 = elo, c2 = (uint32_t)(p0 >> 32) ^ k1t, c3 = (uint32_t)p0;
+#pragma unroll
+    for (int r = 1; r < 10; ++r) philox_round(c0, c1, c2, c3, rk0[r], rk1[r]);
+    return Philox4{c0, c1, c2, c3};
+  }
+
   __device__ __forceinline__ Philox4 operator()(uint32_t c, uint32_t sel) const { return with_tag(c, sel, k1_tag); }
 
   // same stream family with another tag: k1t = seed_hi ^ tag
@@ -135,6 +144,13 @@ __device__ __forceinline__ float unit24_open(uint32_t x) {
 __device__ __forceinline__ float neg_log_u1(uint32_t seed_lo, uint32_t seed_hi, uint32_t s, uint32_t epoch) {
   const Philox4 t = philox4x32_10(0u, s, epoch, kTagTau, seed_lo, seed_hi);
   return -logf(unit24_open(t.x));
+}
+
+// The same -ln(u1) from a TrialStream of the same seed (any tag; its round keys are already
+// in registers, so the call skips the key schedule -- ~16 instructions per tau): counter
+// {0, s, epoch, kTagTau} with sel / elo the stream's round-1 words of (s, epoch).
+__device__ __forceinline__ float neg_log_u1_ts(const TrialStream& ts, uint32_t sel, uint32_t elo) {
+  return -logf(unit24_open(ts.call_tag(0u, sel, elo, ts.rk1[0] ^ kTagTau).x));
 }
 
 // amax >= 2^-102  <=>  amax * 2^-24 is a normal binary32 (exact scaling)
