@@ -409,11 +409,20 @@ __device__ __forceinline__ void lane_loop(const SharedParams& P, const TrialStre
       a2 = (c + 1u < calls) & accept<PATH>(y.y, j2, sbase, P.thr, P.group_shift);
       a3 = (c + 1u < half) & accept<PATH>(y.w, j3, sbase, P.thr, P.group_shift);
     }
-    const bool done = active & (a0 | a1 | a2 | a3 | (c + (uint32_t)NC >= calls));
+    const bool acc = a0 | a1 | a2 | a3;
+    const bool done = active & (acc | (c + (uint32_t)NC >= calls));
     if (done) {
-      idx_out[my] = a0 ? (int32_t)j0 : a1 ? (int32_t)j1 : a2 ? (int32_t)j2 : a3 ? (int32_t)j3 : -1;
-      if constexpr (WANT_TR)
-        tr_out[my] = a0 ? 2u * c + 1u : a1 ? 2u * c + 2u : a2 ? 2u * c + 3u : a3 ? 2u * c + 4u : P.max_trials;
+      // branch-free: the first accepting trial k of the round (a0 first) -> j_k, trials 2c + 1 + k
+      uint32_t k, jk;
+      if constexpr (NC == 1) {
+        k = a0 ? 0u : 1u;
+        jk = a0 ? j0 : j1;
+      } else {
+        k = a0 ? 0u : a1 ? 1u : a2 ? 2u : 3u;
+        jk = a0 ? j0 : a1 ? j1 : a2 ? j2 : j3;
+      }
+      idx_out[my] = acc ? (int32_t)jk : -1;
+      if constexpr (WANT_TR) tr_out[my] = acc ? 2u * c + 1u + k : P.max_trials;
       active = false;
     }
     c += NC;
