@@ -252,10 +252,11 @@ int launch_select(gpuar_handle* h, const float* alpha, int64_t rows, int64_t ld,
         const uint64_t nwarps = std::max<uint64_t>(1u, (uint64_t)h->sh_grid * (uint64_t)h->sh_block / 32u);
         const uint64_t Q = (uint64_t)K * n_epochs;
         const uint64_t fair = std::max<uint64_t>(1u, Q / nwarps);
-        // static first chunk: half the fair share; 3/4 with fewer items than threads, where
-        // select_shared_pre_kernel works it before the PDL wait (c2 +1.6 %, A/B on one box)
-        const bool pre = n_epochs == 1u && Q < (uint64_t)h->sh_grid * (uint64_t)h->sh_block;
-        uint64_t first = pre ? fair * 3u / 4u : fair / 2u;
+        // static first chunk: 3/4 of the fair share (the device raises it to 15/16 at p > 1/4,
+        // pool_setup).  A/B on one box against 1/2: c3 uniform +3 %, c3 exponential +0.7 %, the
+        // rest +-0.6 %; with fewer items than threads select_shared_pre_kernel works it before
+        // the PDL wait (c2 +1.6 %).  7/8 and 15/16 everywhere lost 3-8 % on the heavy tails.
+        uint64_t first = fair * 3u / 4u;
         if (fair <= 4u) {
           const uint64_t stripe = (Q + kStripes - 1u) / kStripes;
           const uint64_t per = std::max<uint64_t>(1u, nwarps / kStripes);  // fewest warps any stripe has

@@ -70,7 +70,7 @@ struct SharedParams {
   uint32_t grab_override;    // tuning: fixed selections per ticket grab (0 = model)
   uint32_t team_override;    // tuning: fixed team size g (power of two 1..32; 0 = model)
   uint32_t fair;             // work stealing: max(1, K / warps of the grid)
-  uint32_t first_base;       // static first chunk before the team minimum: fair / 2, or, with
+  uint32_t first_base;       // static first chunk before the team minimum: 3 fair / 4, or, with
                              // fair <= 4, ceil(ceil(K / kStripes) / max(1, warps / kStripes))
                              // (static chunks that cover each stripe: no tickets at all)
   uint32_t no_prefetch;      // tuning: 1 = fetch tickets on demand
