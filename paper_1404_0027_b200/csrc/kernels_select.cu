@@ -556,8 +556,10 @@ __device__ __forceinline__ void pool_setup(const SharedParams& P, const DevStats
   // +2 % over 3/4; at heavy tails 15/16 lost 3-8 %)
   const unsigned long long fb = (st.p > 0.25f && fair > 4u) ? fair - fair / 16u : P.first_base;
   const unsigned long long first = max(teams, fb);
-  // (r01 sweep, GPUAR_GRAB: c2 best at 2 with prefetch; heavy tails (st.grab = 1) at 1)
-  unsigned long long grab = max(teams, min((unsigned long long)st.grab, max(2ull * teams, fair / 8ull)));
+  // (r01 sweep, GPUAR_GRAB: c2 best at 2 with prefetch; heavy tails (st.grab = 1) at 1;
+  // session 4: the two-call lane loop best at one selection per lane, c3 Pareto +2.6-2.9 %)
+  const unsigned long long two_min = (g == 1u && st.p <= 0.25f) ? 1ull : 2ull;
+  unsigned long long grab = max(teams, min((unsigned long long)st.grab, max(two_min * teams, fair / 8ull)));
   if (P.grab_override) grab = P.grab_override;
 #ifdef GPUAR_TIMELINE
   pl.tl_slot = P.epoch & 1u;
