@@ -51,6 +51,39 @@ __device__ __forceinline__ bool accept(uint32_t x, uint32_t j, uint32_t sbase, c
   }
 }
 
+// Both trials of a Philox call (words (x.y, j0) and (x.w, j1)) for the whole warp.  On the
+// prefilter paths the 16-bit test decides all but a rare few trials (a bracket tie, 2^-16 per
+// trial on path 2; h <= the group bound on path 3); those read the exact T_j from L2 under one
+// warp vote instead of as predicated instructions every trial (~10 issue slots per round).
+// Every lane of the warp must call it (it votes).
+template <int PATH>
+__device__ __forceinline__ void accept2(uint32_t xy, uint32_t j0, uint32_t xw, uint32_t j1, uint32_t sbase,
+                                        const uint32_t* __restrict__ thr, uint32_t group_shift, bool& r0, bool& r1) {
+  if constexpr (PATH == kPathSmemF32) {
+    r0 = accept<PATH>(xy, j0, sbase, thr, group_shift);
+    r1 = accept<PATH>(xw, j1, sbase, thr, group_shift);
+  } else {
+    const uint32_t h0 = xy >> 16, h1 = xw >> 16;
+    bool u0, u1;
+    if constexpr (PATH == kPathSmemBf16) {
+      const uint32_t b0 = lds_u16(sbase + 2u * j0), b1 = lds_u16(sbase + 2u * j1);
+      r0 = h0 < b0;
+      r1 = h1 < b1;
+      u0 = h0 == b0;
+      u1 = h1 == b1;
+    } else {
+      u0 = h0 <= lds_u16(sbase + 2u * (j0 >> group_shift));
+      u1 = h1 <= lds_u16(sbase + 2u * (j1 >> group_shift));
+      r0 = false;
+      r1 = false;
+    }
+    if (__any_sync(kFull, u0 | u1)) {
+      if (u0) r0 = (xy >> 8) < __ldg(thr + j0);
+      if (u1) r1 = (xw >> 8) < __ldg(thr + j1);
+    }
+  }
+}
+
 // Round-1 words of work item q: selection s0 + q at the launch's epoch, or (multi-epoch
 // launch) selection s0 + q mod Ksel at epoch + q / Ksel.  elo is lo(M1 * epoch).
 template <bool MULTI>
@@ -238,8 +271,8 @@ __device__ __forceinline__ void trial_loop(const SharedParams& P, const TrialStr
       j0 = __umulhi(x.x, M);
       j1 = __umulhi(x.z, M);
       // branch-free: both gathers always issue (j < M is always a valid index)
-      const bool r0 = accept<PATH>(x.y, j0, sbase, P.thr, P.group_shift);
-      const bool r1 = accept<PATH>(x.w, j1, sbase, P.thr, P.group_shift);
+      bool r0, r1;
+      accept2<PATH>(x.y, j0, x.w, j1, sbase, P.thr, P.group_shift, r0, r1);
       a0 = active & (c < calls) & r0;
       a1 = active & (c < half) & r1;
       ball = __ballot_sync(kFull, a0 || a1);
@@ -289,8 +322,10 @@ __device__ __forceinline__ void warp_rounds(const SharedParams& P, const TrialSt
     const Philox4 x = item_call<MULTI>(ts, c, sel, elo);
     const uint32_t j0 = __umulhi(x.x, M);
     const uint32_t j1 = __umulhi(x.z, M);
-    const bool a0 = (c < calls) & accept<PATH>(x.y, j0, sbase, P.thr, P.group_shift);
-    const bool a1 = (c < half) & accept<PATH>(x.w, j1, sbase, P.thr, P.group_shift);
+    bool r0, r1;
+    accept2<PATH>(x.y, j0, x.w, j1, sbase, P.thr, P.group_shift, r0, r1);
+    const bool a0 = (c < calls) & r0;
+    const bool a1 = (c < half) & r1;
     const uint32_t b = __ballot_sync(kFull, a0 || a1);
     if (b != 0u) {
       const uint32_t w = __ffs(b) - 1;
@@ -396,8 +431,8 @@ __device__ __forceinline__ void lane_loop(const SharedParams& P, const TrialStre
     const Philox4 x = item_call<MULTI>(ts, c, sel, elo);
     const uint32_t j0 = __umulhi(x.x, M);
     const uint32_t j1 = __umulhi(x.z, M);
-    const bool r0 = accept<PATH>(x.y, j0, sbase, P.thr, P.group_shift);
-    const bool r1 = accept<PATH>(x.w, j1, sbase, P.thr, P.group_shift);
+    bool r0, r1;
+    accept2<PATH>(x.y, j0, x.w, j1, sbase, P.thr, P.group_shift, r0, r1);
     const bool a0 = (c < calls) & r0;
     const bool a1 = (c < half) & r1;
     bool a2 = false, a3 = false;
@@ -406,8 +441,10 @@ __device__ __forceinline__ void lane_loop(const SharedParams& P, const TrialStre
       const Philox4 y = item_call<MULTI>(ts, c + 1u, sel, elo);
       j2 = __umulhi(y.x, M);
       j3 = __umulhi(y.z, M);
-      a2 = (c + 1u < calls) & accept<PATH>(y.y, j2, sbase, P.thr, P.group_shift);
-      a3 = (c + 1u < half) & accept<PATH>(y.w, j3, sbase, P.thr, P.group_shift);
+      bool r2, r3;
+      accept2<PATH>(y.y, j2, y.w, j3, sbase, P.thr, P.group_shift, r2, r3);
+      a2 = (c + 1u < calls) & r2;
+      a3 = (c + 1u < half) & r3;
     }
     const bool acc = a0 | a1 | a2 | a3;
     const bool done = active & (acc | (c + (uint32_t)NC >= calls));
@@ -452,8 +489,8 @@ __device__ __forceinline__ void warp_select(const SharedParams& P, const TrialSt
     const Philox4 x = item_call<MULTI>(ts, c, sel, elo);
     const uint32_t j0 = __umulhi(x.x, M);
     const uint32_t j1 = __umulhi(x.z, M);
-    const bool r0 = accept<PATH>(x.y, j0, sbase, P.thr, P.group_shift);
-    const bool r1 = accept<PATH>(x.w, j1, sbase, P.thr, P.group_shift);
+    bool r0, r1;
+    accept2<PATH>(x.y, j0, x.w, j1, sbase, P.thr, P.group_shift, r0, r1);
     const bool a0 = (!decltype(cap)::value || c < calls) & r0;
     const bool a1 = (!decltype(cap)::value || c < half) & r1;
     const uint32_t b = __ballot_sync(kFull, a0 || a1);
