@@ -15,7 +15,12 @@
 //  * teams that finish take the next selection from a warp-local pool refilled from one of
 //    64 striped tickets (one 64-bit atomic per `grab` selections, prefetched one chunk
 //    ahead): work stealing, so geometric trial counts leave no long tail;
-//  * tau is a separate, fully coalesced grid-stride phase;
+//  * when a lane-loop warp's pool is dry, the whole warp finishes its last selections one at
+//    a time (warp_rounds, the endgame);
+//  * tau is a separate, fully coalesced grid-stride phase, drawn on the
+//    trial stream's round keys, partly before the programmatic-dependent-launch wait;
+//  * with fewer work items than threads, select_shared_pre_kernel lets whole-warp teams work
+//    their static chunk before that wait instead;
 //  * MULTI: one launch works n consecutive selects (gpuar_select_epochs): the work items are
 //    the n*K (epoch, selection) pairs, item q -> selection q mod K at epoch + q / K, output
 //    slot q.
