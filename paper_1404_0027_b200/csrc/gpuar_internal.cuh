@@ -308,6 +308,18 @@ __device__ __forceinline__ float2 fadd2_rn(float2 a, float2 b) {
   return d;
 }
 
+// RN(t / d) from the correctly rounded reciprocal y = RN(1/d): q0 = RN(t y), r = t - d q0
+// (exact with an FMA), q = RN(q0 + r y) -- the final correction of IEEE division by
+// Newton-Raphson with an FMA (Markstein), which returns the correctly rounded quotient when
+// nothing underflows or overflows (checked exhaustively over all 2^46 significand pairs,
+// DESIGN.md R23); the caller guarantees the exponent range, so this is bit-identical to
+// __fdiv_rn(t, d) at 3 instead of ~8 instructions (no MUFU.RCP, no reciprocal refinement,
+// no FCHK slow-path test).  Used by the argmin rule's ratings and the shared-vector tau.
+__device__ __forceinline__ float div_by_recip(float t, float d, float y) {
+  const float q0 = __fmul_rn(t, y);
+  return __fmaf_rn(__fmaf_rn(-q0, d, t), y, q0);
+}
+
 __device__ __forceinline__ uint32_t lanemask_lt() {
   uint32_t m;
   asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));

@@ -23,17 +23,6 @@ namespace gpuar {
 
 namespace {
 
-// The rating RN(t / d) with the reaction's correctly rounded reciprocal y = RN(1/d) staged
-// beside it: q0 = RN(t y), r = t - d q0 (exact with an FMA), q = RN(q0 + r y) -- the final
-// correction of IEEE division by Newton-Raphson with an FMA (Markstein), which returns the
-// correctly rounded quotient when nothing underflows or overflows; the caller guarantees
-// that (R23), so this is bit-identical to __fdiv_rn(t, d) at 3 instead of ~8
-// instructions (no MUFU.RCP, no reciprocal refinement, no FCHK slow-path test).
-__device__ __forceinline__ float div_by_recip(float t, float d, float y) {
-  const float q0 = __fmul_rn(t, y);
-  return __fmaf_rn(__fmaf_rn(-q0, d, t), y, q0);
-}
-
 // election: eligible iff t < d (d = 0 is never eligible since t >= 0), rating t / d; a
 // lane sees its reactions in increasing j, so a strict `<` keeps the lowest index on ties.
 template <bool FASTDIV>

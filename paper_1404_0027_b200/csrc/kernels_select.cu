@@ -104,6 +104,20 @@ __device__ __forceinline__ void item_words(const SharedParams& P, const TrialStr
   }
 }
 
+// tau = -ln(u1) / fl32(alpha_0) (R10) in binary32, IEEE division:
+// by the staged reciprocal (div_by_recip, bit-identical) when 2^-60 <= fl32(alpha_0) <= 2^60
+// -- then -ln(u1) in [2^-24, 16.7] keeps every quotient and residual normal -- else __fdiv_rn.
+struct TauDiv {
+  float a0f, ra0;
+  bool fast;
+  __device__ __forceinline__ float operator()(float nl) const {
+    return fast ? div_by_recip(nl, a0f, ra0) : __fdiv_rn(nl, a0f);
+  }
+};
+__device__ __forceinline__ TauDiv tau_div(float a0f) {
+  return TauDiv{a0f, __frcp_rn(a0f), a0f >= 0x1p-60f && a0f <= 0x1p60f};
+}
+
 // -ln(u1) of work item q's tau (R10) from the trial stream's keys
 template <bool MULTI>
 __device__ __forceinline__ float item_neg_log_u1(const SharedParams& P, const TrialStream& ts, uint32_t q) {
@@ -672,6 +686,7 @@ __global__ void __launch_bounds__(1024, 1) select_shared_kernel(const SharedPara
   const uint32_t K = P.K;
   const uint32_t nwarps = nthreads >> 5;
   const TrialStream ts(P.seed_lo, P.seed_hi, P.epoch);  // (also tau's round keys)
+  const TauDiv tdiv = tau_div(st.a0f);
   if (threadIdx.x == 0) s_g = P.team_override ? P.team_override : choose_team(st.p, K, nwarps);  // once per CTA
   // tau of this thread's first kPreTau selections, computed before the wait (pure arithmetic
   // on the statistics) and stored after it: on an SM the previous call left early this work
@@ -684,7 +699,7 @@ __global__ void __launch_bounds__(1024, 1) select_shared_kernel(const SharedPara
   for (uint32_t i = 0; i < kPreTau; ++i) {
     const uint32_t s = tid + i * nthreads;
     pre_tau[i] = 0.f;
-    if (want_tau && s < K) pre_tau[i] = __fdiv_rn(item_neg_log_u1<MULTI>(P, ts, s), st.a0f);
+    if (want_tau && s < K) pre_tau[i] = tdiv(item_neg_log_u1<MULTI>(P, ts, s));
   }
   // every prerequisite grid complete; then let the next launch be scheduled early
   pdl_wait();
@@ -710,7 +725,7 @@ __global__ void __launch_bounds__(1024, 1) select_shared_kernel(const SharedPara
       if (P.trials) P.trials[s] = 0u;
       if (P.tau) P.tau[s] = invalid ? __uint_as_float(0x7fc00000u) : __uint_as_float(kInfBits);
     } else if (P.tau) {
-      P.tau[s] = __fdiv_rn(item_neg_log_u1<MULTI>(P, ts, s), st.a0f);
+      P.tau[s] = tdiv(item_neg_log_u1<MULTI>(P, ts, s));
     }
   }
   __syncthreads();        // publishes the barrier's initialisation and s_g
@@ -773,6 +788,7 @@ __global__ void __launch_bounds__(1024, 1) select_shared_pre_kernel(const Shared
   Pool pl;
   pool_setup(P, st, g, nwarps, warp_global, pl);
   const TrialStream ts(P.seed_lo, P.seed_hi, P.epoch);
+  const TauDiv tdiv = tau_div(st.a0f);
   uint32_t pre_n = 0;
   const uint32_t pre_base = pl.next;
   int32_t pre_id = -1;
@@ -805,7 +821,7 @@ __global__ void __launch_bounds__(1024, 1) select_shared_pre_kernel(const Shared
       if (P.trials) P.trials[s] = 0u;
       if (P.tau) P.tau[s] = invalid ? __uint_as_float(0x7fc00000u) : __uint_as_float(kInfBits);
     } else if (P.tau) {
-      P.tau[s] = __fdiv_rn(item_neg_log_u1<false>(P, ts, s), st.a0f);
+      P.tau[s] = tdiv(item_neg_log_u1<false>(P, ts, s));
     }
   }
   if (invalid || zero) return;  // uniform over the grid; the tickets are untouched
