@@ -709,6 +709,18 @@ def run_gpuar(args, w, rank, world, local_rank):
                     "bytes_per_selection": 4 * M + 12, "frac_of_8TBs": achieved / 8000.0,
                     "row_stats_stream_gbs": rs_gbs, "row_stats_stream_sustained": rs_sus,
                     "per": "rank 0's launches (CUDA events on its stream)"}
+        if w["rule"] == "argmin":
+            # the paper's rule draws ceil(M/4) Philox calls per row (plus one for tau): ALU-bound,
+            # so its roofline is the Philox peak; the HBM fraction stays beside it
+            mhz = float(peaks.get("sm_max_mhz", 1965.0))
+            alu_peak = SM_COUNT * FMA_SLOTS_PER_CLK_PER_SM / FMA_SLOTS_PER_PHILOX * mhz * 1e6 / 1e9
+            alu_ach = K * ((M + 3) // 4 + 1) / (ms_rank_step * 1e-3) / 1e9
+            hbm = {k: roofline[k] for k in ("achieved", "peak", "unit", "frac", "peak_source", "bytes_per_selection")}
+            roofline = {"bound": "alu", "achieved": alu_ach, "peak": alu_peak, "unit": "G Philox calls/s",
+                        "frac": alu_ach / alu_peak, "traffic": None,
+                        "peak_source": f"148 SM x 64 fma-pipe slots/clk / (20 IMAD.WIDE x 2 slots) per Philox4x32-10 x {mhz:.0f} MHz",
+                        "calls_per_selection": (M + 3) // 4 + 1, "hbm": hbm,
+                        "per": "rank 0's launches (CUDA events on its stream)"}
         if sustained:
             sustained["roofline_frac"] = K * (4 * M + 12) / (sus_ms_rank / sustained["steps"] * 1e-3) / 1e9 / peak
             if rs_sus:
