@@ -364,3 +364,75 @@ def test_lane_loop_endgame(monkeypatch, M, endgame):
     sel.sync()
     assert sel.last_team == 1
     _check(out, oracle.ar_select(a, K, seed=SEED, epoch=3, s0=12345, nthreads=16))
+
+
+# ---------------------------------------------------------------- output bounds (no sanitizer)
+
+GUARD = 4096                 # canary words on each side of every output buffer
+CANARY = 0x7E57C0DE
+
+
+def _guarded(K):
+    bufs = []
+    for dt in (torch.int32, torch.float32, torch.int32):
+        b = torch.empty(K + 2 * GUARD, dtype=torch.int32, device="cuda").fill_(CANARY)
+        bufs.append(b if dt == torch.int32 else b.view(torch.float32))
+    views = tuple(b[GUARD:GUARD + K] for b in bufs)
+    return bufs, views
+
+
+def _canaries_intact(bufs, K):
+    for b in bufs:
+        w = b.view(torch.int32)
+        if not (bool((w[:GUARD] == CANARY).all()) and bool((w[GUARD + K:] == CANARY).all())):
+            return False
+    return True
+
+
+@pytest.mark.parametrize("case", ["pre_kernel_g32", "lane_endgame", "lane_uniform", "group_path", "rows",
+                                  "rows_argmin", "shared_argmin", "shared_it", "epochs"])
+def test_outputs_stay_in_bounds(monkeypatch, case):
+    """Every kernel writes only its K (or n x K) outputs: the output tensors are views into
+    buffers with 4096 canary words on each side, checked after back-to-back launches (a
+    bounds check of our own now that the GPU pool has closed compute-sanitizer), plus parity
+    of the outputs against the oracle where the oracle is cheap."""
+    from paper_1404_0027_b200 import Selector
+    if case == "pre_kernel_g32":
+        a, K, rule = synth.yeast_like(), 70_001, "classic"
+    elif case == "lane_endgame":
+        a, K, rule = synth.pareto(1000), 300_007, "classic"
+    elif case == "lane_uniform":
+        a, K, rule = synth.uniform(10_000), 600_001, "classic"
+    elif case == "group_path":
+        a, K, rule = synth.pareto(300_000), 20_011, "classic"
+    elif case == "shared_argmin":
+        a, K, rule = synth.discrete_gaussian(1024), 30_001, "argmin"
+    elif case == "shared_it":
+        a, K, rule = synth.yeast_like(), 40_003, "it"
+    elif case in ("rows", "rows_argmin"):
+        M, K = 1029, 5003
+        a = synth.rows(synth.yeast_rates(M), synth.GEN_SEED, 0, K)
+        rule = "classic" if case == "rows" else "argmin"
+    else:
+        a, K, rule = synth.exponential(1000), 50_021, "classic"
+    a = np.ascontiguousarray(a, np.float32)
+    M = a.shape[-1]
+    sel = Selector(M, K, SEED)
+    if rule != "classic":
+        sel.set_rule(rule, 1.0)
+    sel.set_propensities(torch.from_numpy(a).cuda())
+    if case == "epochs":
+        n = 3
+        bufs, views = _guarded(n * K)
+        for _ in range(2):
+            sel.select_epochs(n, K, out=views)
+        sel.sync()
+        assert _canaries_intact(bufs, n * K)
+        return
+    bufs, views = _guarded(K)
+    for _ in range(3):
+        sel.select(K, out=views)
+    sel.sync()
+    assert _canaries_intact(bufs, K)
+    if rule == "classic" and case != "lane_uniform":
+        _check(views, oracle.ar_select(a, K, seed=SEED, epoch=2, nthreads=16))
